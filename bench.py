@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""STTSV bench: hyperedge-vertex incidences/s of y = B x^{N-1} on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config large] [--impl ours|reference]
+
+One step = one sttsv_apply over the whole configured workload (gather ->
+edge kernel -> [NCCL allreduce of y_active] -> expand), inputs resident in
+HBM.  At N=1 the workload is BASELINE.json's `large` config (1e8 hyperedges,
+rank 8, n = 1e7; the largest config that fits one GPU); for
+N>1 the same edge list is sharded over the ranks (strong scaling) with one
+NCCL allreduce of y_active per step.  Prints ONE JSON line on rank 0.
+
+--impl reference times the CPU oracle (oracle/, the plain kappa-enumeration
+definition) on the host cores, each step a bounded deterministic sample of
+the same workload; it is the reference arm of this tier (no installable
+reference implementation exists: the paper ships no code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "STTSV hyperedge-vertex incidences/sec"
+UNIT = "incidences/s"
+FALLBACK_HBM_GBS = 6650.0     # B200_PROFILING.md fallback
+FP64_MEASURED = os.path.join(ROOT, "profiles", "r01_fp64_peaks.txt")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback 6.65 TB/s from B200_PROFILING.md"
+
+
+def fp64_peak_tflops():
+    try:
+        for line in open(FP64_MEASURED):
+            if line.startswith("DFMA:"):
+                return float(line.split()[1]), "measured DFMA microbenchmark (tools/fp64_peaks.cu)"
+    except Exception:
+        pass
+    return 37.2, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
+def ncu_traffic(config):
+    """dram bytes per edge-kernel launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_edge_kernel.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        if d.get("config") == config:
+            return d.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            log("clock sampler unavailable:", e)
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- CPU oracle
+def oracle_sample(hg, target_s, calib_edges=20_000):
+    """Time the oracle (as it stands) on a deterministic every-s-th-edge sample
+    sized for about target_s seconds; returns (incidences/s, seconds, sample desc, threads)."""
+    import oracle
+    calib = hg.subset(np.arange(0, hg.m, max(1, hg.m // calib_edges)))
+    t0 = time.perf_counter()
+    oracle.sttsv(calib)
+    rate = calib.incidences / max(time.perf_counter() - t0, 1e-6)
+    want = max(1000, int(rate * target_s))
+    stride = max(1, hg.incidences // want)
+    sub = hg.subset(np.arange(0, hg.m, stride))
+    t0 = time.perf_counter()
+    oracle.sttsv(sub)
+    dt = time.perf_counter() - t0
+    desc = (f"every {stride}-th edge of '{hg.config}' ({sub.m} edges, {sub.incidences} incidences, "
+            f"full n={hg.n}); oracle = kappa-enumeration in long double, OpenMP")
+    return sub.incidences / dt, dt, desc, oracle.num_threads(), sub
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    hg = W.generate(args.config)
+    total = args.steps + args.warmup
+    per_step = min(10.0, max(0.5, 150.0 / max(total, 1)))
+    rate0, _, desc, threads, sub = oracle_sample(hg, per_step)
+    times = []
+    for i in range(total):
+        t0 = time.perf_counter()
+        oracle.sttsv(sub)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    dt = sum(times) / max(len(times), 1)
+    value = sub.incidences / dt
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank,
+                      "sample_incidences_per_step": sub.incidences},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2311_08595_b200 as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    t0 = time.perf_counter()
+    hg = W.generate(args.config)
+    log(f"[rank {rank}] generated {args.config}: m={hg.m} incidences={hg.incidences} in {time.perf_counter()-t0:.1f}s")
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(S.sttsv_comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0)
+        comm = S.sttsv_comm_create(bytes(uid.cpu().tolist()), world, rank, local)
+    t0 = time.perf_counter()
+    plan = S.Plan.from_hypergraph(hg, device=local, world=world, rank=rank, comm=comm)
+    info = plan.info()
+    log(f"[rank {rank}] plan in {time.perf_counter()-t0:.1f}s: {json.dumps({k: v for k, v in info.items() if k != 'edges_per_size'})}")
+
+    x = torch.from_numpy(hg.x).to(dev)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        plan.apply(x, y, stream)
+    barrier()
+    sampler = ClockSampler(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        plan.profile(True)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.apply(x, y, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        plan.profile(False)
+    ms_total = ev0.elapsed_time(ev1)
+    kern_ms, kern_n = plan.profile_read()
+    kern_avg = kern_ms / max(kern_n, 1)
+    if world > 1:
+        t = torch.tensor([ms_total, kern_avg], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, kern_avg = t.tolist()
+    ms_step = ms_total / args.steps
+    value = hg.incidences / (ms_step * 1e-3)
+
+    # ---------------- end to end through the public host-buffer call (sttsv_apply_host)
+    xh = torch.from_numpy(hg.x.copy()).pin_memory()
+    yh = torch.empty(hg.n, dtype=torch.float64).pin_memory()
+    xh_np, yh_np = xh.numpy(), yh.numpy()
+    plan.apply_host(xh_np, yh_np)
+    e2e_steps = max(1, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.apply_host(xh_np, yh_np)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
+    e2e = {"value": hg.incidences / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 8),
+           "d2h_bytes_per_step": int(yh.numel() * 8), "ms_per_step": e2e_s * 1e3,
+           "timing": "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
+
+    # ---------------- roofline of the dominant kernel (edge kernel)
+    alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
+    fp64_peak, fp64_src = fp64_peak_tflops()
+    fp64_tf = 2.0 * info["fma_per_apply"] / (kern_avg * 1e-3) / 1e12
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config), "kernel": "sttsv::edge_kernel<N>",
+                "kernel_ms": kern_avg, "kernel_share_of_step": kern_avg / ms_step,
+                "alg_bytes_per_launch": alg_bytes,
+                "alg_bytes_def": "4*sum|e| (int32 ids) + 8*m (fp64 w') + 8*n_active (x_a) + 8*n_active (y_a) per shard",
+                "peak_source": peak_src,
+                "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_tf / fp64_peak,
+                         "peak_source": fp64_src,
+                         "flops_def": "2 x FMAs of the per-edge DP incl. series generation (SURVEY.md App. A)"}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, dt, desc, threads, _ = oracle_sample(hg, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+               "seconds": dt}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": args.config, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank,
+                          "incidences": hg.incidences, "n_active": info["n_active"],
+                          "l2": "inputs larger than L2: the %.2f GB edge stream is read once per step"
+                                % (info["stream_bytes"] * world / 1e9),
+                          "parallelism": "edge-sharded x%d%s" % (world, " + NCCL allreduce of y_active"
+                                                                 if world > 1 else ""),
+                          "kernel_grid": info["kernel_grid"], "kernel_block": info["kernel_block"],
+                          "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
+                          / (ms_step * 1e-3) / 1e9},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": plan.launches() * args.steps, "clocks": sampler.summary()}
+        print(json.dumps(out), flush=True)
+    plan.close()
+    if comm is not None:
+        S.sttsv_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="large", choices=sorted(W.CONFIGS))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: raising --warmup to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

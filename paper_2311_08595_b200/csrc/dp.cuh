@@ -1,0 +1,115 @@
+// dp.cuh — per-edge coefficient DP of the blowup STTSV (row a3 of SURVEY.md §8(a)).
+//
+// For an edge e = {u_0..u_{K-1}} and global rank N, Alg. 2
+// gives member v the coefficient
+//     (N-1)! [t^{N-1}]  e^{x_v t} prod_{u in e\v} (e^{x_u t} - 1)
+// (E_N / Ebar_N are the truncated EGFs of e^{ct} and e^{ct}-1),
+// to be scaled by w(e)/|beta(e)|.  Write
+//     e^{x t} - 1 = t g(t),   g[j] = x^{j+1}/(j+1)!   (j >= 0)
+// and e^{x_v t} = 1 + t g_v(t).  Then, with D = N - K,
+//     [t^{N-1}] e^{x_v t} prod_{u!=v} (e^{x_u t}-1) = [t^D] prod_{u!=v} g_u  +  [t^{D-1}] prod_u g_u
+//                                                   =        Q_v[D]          +       F[D-1].
+// Only coefficients 0..D of each g are ever needed (L = D + 1 of them), and
+// every term is a product of positive numbers when x > 0 (no cancellation).
+// Q_v = P_{i-1} S_{i+1} with prefix products P_i = g_0..g_i and suffix products
+// S_i = g_i..g_{K-1}; [t^D] of a product is a length-L dot product.
+//
+// dp_edge<K, L> returns c_i = Q_{u_i}[D] + F[D-1]  (WITHOUT the (N-1)!/|beta|
+// factor: the planner folds (N-1)!/|beta(K)| into the stored weight w').
+// All loops are over compile-time bounds, so the arrays live in registers.
+#pragma once
+
+namespace sttsv {
+
+__device__ __forceinline__ constexpr double inv_fact_c(int j) {
+  double f = 1.0;
+  for (int i = 2; i <= j; ++i) f *= double(i);
+  return 1.0 / f;
+}
+
+// truncated product r = (a*b) mod t^L
+template <int L>
+__device__ __forceinline__ void trunc_mul(const double (&a)[L], const double (&b)[L], double (&r)[L]) {
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s = a[0] * b[j];
+#pragma unroll
+    for (int i = 1; i <= j; ++i) s = fma(a[i], b[j - i], s);
+    r[j] = s;
+  }
+}
+
+// [t^D] (a*b) over the first D+1 coefficients
+template <int D, int L>
+__device__ __forceinline__ double coef(const double (&a)[L], const double (&b)[L]) {
+  static_assert(D < L, "coef degree");
+  double s = a[0] * b[D];
+#pragma unroll
+  for (int j = 1; j <= D; ++j) s = fma(a[j], b[D - j], s);
+  return s;
+}
+
+template <int K, int L>
+__device__ __forceinline__ void dp_edge(const double (&x)[K], double (&c)[K]) {
+  constexpr int D = L - 1;
+  if constexpr (K == 1) {
+    // singleton: Q = 1 (empty product), F = g_0:  c = [D==0] + g_0[D-1] = x^{N-1}/(N-1)!
+    if constexpr (D == 0) {
+      c[0] = 1.0;
+    } else {
+      double pw = x[0];
+#pragma unroll
+      for (int j = 1; j < D; ++j) pw *= x[0];
+      c[0] = pw * inv_fact_c(D);
+    }
+  } else {
+    double g[K][L];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double pw = x[i];
+      g[i][0] = pw;
+#pragma unroll
+      for (int j = 1; j < L; ++j) {
+        pw *= x[i];
+        g[i][j] = pw * inv_fact_c(j + 1);
+      }
+    }
+    if constexpr (K == 2) {
+      double F = 0.0;
+      if constexpr (D >= 1) F = coef<D - 1, L>(g[0], g[1]);
+      c[0] = g[1][D] + F;
+      c[1] = g[0][D] + F;
+    } else {
+      // prefixes P[i] = g_0 * ... * g_i, i = 0..K-3
+      double P[K - 2][L];
+#pragma unroll
+      for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
+#pragma unroll
+      for (int i = 1; i <= K - 3; ++i) trunc_mul<L>(P[i - 1], g[i], P[i]);
+      // last two members
+      c[K - 1] = coef<D, L>(P[K - 3], g[K - 2]);   // [t^D] P_{K-2}
+      c[K - 2] = coef<D, L>(P[K - 3], g[K - 1]);   // [t^D] P_{K-3} S_{K-1}
+      double S[L];
+      trunc_mul<L>(g[K - 2], g[K - 1], S);          // S_{K-2}
+      double F = 0.0;
+      if constexpr (D >= 1) F = coef<D - 1, L>(P[K - 3], S);   // [t^{D-1}] P_{K-3} S_{K-2}
+#pragma unroll
+      for (int i = K - 3; i >= 1; --i) {
+        c[i] = coef<D, L>(P[i - 1], S);            // [t^D] P_{i-1} S_{i+1}
+        if (i > 1) {
+          double T[L];
+          trunc_mul<L>(g[i], S, T);                 // S_i
+#pragma unroll
+          for (int j = 0; j < L; ++j) S[j] = T[j];
+        } else {
+          c[0] = coef<D, L>(g[1], S);               // [t^D] S_1 = [t^D] g_1 S_2
+        }
+      }
+      if constexpr (K == 3) c[0] = S[D];           // S = S_1
+#pragma unroll
+      for (int i = 0; i < K; ++i) c[i] += F;
+    }
+  }
+}
+
+}  // namespace sttsv

@@ -1,0 +1,22 @@
+// edge_inst.cu — one instantiation of edge_kernel<N> per object file (compiled
+// once per rank in STTSV_COMPILED_RANKS with -DSTTSV_INST_N=<N>, and once with
+// N = 0 for the generic kernel), so the build parallelises over ranks.
+#include "edge_kernel.cuh"
+
+#ifndef STTSV_INST_N
+#error "compile with -DSTTSV_INST_N=<rank>"
+#endif
+
+#define STTSV_CAT2(a, b) a##b
+#define STTSV_CAT(a, b) STTSV_CAT2(a, b)
+
+namespace sttsv {
+EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
+  EdgeKernelEntry e;
+  e.fn = (const void*)edge_kernel<STTSV_INST_N>;
+  e.block = EdgeCfg<STTSV_INST_N>::BLOCK;
+  e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::STAGES * EdgeCfg<STTSV_INST_N>::STAGE_BYTES;
+  e.rank = STTSV_INST_N;
+  return e;
+}
+}  // namespace sttsv

@@ -1,0 +1,73 @@
+// internal.h — structures shared by the host planner (plan.cpp) and the CUDA
+// kernels (kernels.cu).  Not part of the public ABI (include/sttsv.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sttsv.h"
+
+namespace sttsv {
+
+// One cardinality bucket of the device hyperedge store:
+// edges of size k, SoA: ids[i * stride + e] is member i (relabelled id, members
+// ascending) of edge e; w[e] = w(e) (N-1)!/|beta(k)| (Alg. 2 factor).
+struct BucketDesc {
+  int32_t k;
+  int32_t pad_;
+  int64_t m;           // edges in this bucket (this shard)
+  int64_t stride;      // column stride of ids (>= m, multiple of 4)
+  int64_t tile_begin;  // first tile of this bucket in the kernel's tile order
+  int64_t ids_off;     // element offset of column 0 in the ids pool
+  int64_t w_off;       // element offset in the weight pool
+};
+
+constexpr int kMaxBuckets = STTSV_MAX_RANK;
+
+struct EdgeKernelParams {
+  int32_t N;             // rank
+  int32_t nb;            // number of non-empty buckets, in tile order
+  BucketDesc b[kMaxBuckets];
+  const int32_t* ids;    // ids pool
+  const double* w;       // weight pool
+  const double* xa;      // x on active vertices (relabelled)
+  double* ya;            // y on active vertices (accumulated)
+  int32_t n_active;
+  int32_t T;             // ids < T: thread-private accumulation slots
+  int32_t H;             // ids < H: CTA shared-memory accumulators
+  int32_t tile_edges;    // edges per tile (= blockDim.x)
+  int64_t num_tiles;
+  int32_t* tile_counter; // dynamic tile scheduler (zeroed before each launch)
+};
+
+// Ranks with a fully unrolled edge kernel (one object file each); every other
+// rank <= STTSV_MAX_RANK runs the generic instantiation (N = 0).
+#define STTSV_COMPILED_RANKS(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(25)
+
+struct EdgeKernelEntry {
+  const void* fn;      // __global__ edge_kernel<N>
+  int block;           // threads per CTA (= edges per tile)
+  size_t ring_bytes;   // shared memory of the TMA ring
+  int rank;            // N of the instantiation (0 = generic)
+};
+#define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry_##n();
+STTSV_COMPILED_RANKS(STTSV_DECLARE_ENTRY)
+EdgeKernelEntry edge_entry_0();
+#undef STTSV_DECLARE_ENTRY
+
+// launchers (kernels.cu)
+EdgeKernelEntry edge_entry(int N);
+// dynamic shared memory of the edge kernel for hot tiers T, H
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int T, int H);
+cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
+cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
+                               cudaStream_t s);
+cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, int64_t n_active, cudaStream_t s);
+cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
+constexpr int kNormalizeScratch = 296;  // doubles of scratch launch_normalize needs
+cudaError_t launch_normalize(const double* z, double* x, double* partial, int64_t n_active, int N,
+                             cudaStream_t s);
+cudaError_t launch_fill_const(double* y, int64_t n, double v, cudaStream_t s);
+
+}  // namespace sttsv

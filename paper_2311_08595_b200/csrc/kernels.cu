@@ -1,0 +1,157 @@
+// kernels.cu — the small kernels of one STTSV apply and the edge-kernel
+// registry (the hot rows a3-a5 live in
+// edge_kernel.cuh, instantiated per rank by edge_inst.cu).
+//
+//   a2 gather      x_a[i] = x[act[i]]                        gather_kernel
+//   a7 expand      y[act[i]] = y_a[i]                        expand_kernel
+//   a8 power step  x_a = z_a^[1/(N-1)] / ||.||_1              normalize_{partial,apply}_kernel
+//      (Alg. 1 line 6)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "edge_kernel.cuh"
+#include "internal.h"
+
+namespace sttsv {
+
+// ------------------------------------------------------- small kernels
+__global__ void gather_kernel(const double* __restrict__ x, const int32_t* __restrict__ act,
+                              double* __restrict__ xa, int64_t n_active) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
+       i += (int64_t)gridDim.x * blockDim.x)
+    xa[i] = x[act[i]];
+}
+
+__global__ void expand_kernel(const double* __restrict__ ya, const int32_t* __restrict__ act,
+                              double* __restrict__ y, int64_t n_active) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[act[i]] = ya[i];
+}
+
+__global__ void fill_kernel(double* __restrict__ y, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = v;
+}
+
+constexpr int kNormBlock = 1024;
+constexpr int kNormMaxGrid = kNormalizeScratch;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (warp == 0) {
+    s = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[0] = s;
+  }
+  __syncthreads();
+  s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// r_i = z_i^{1/(N-1)} into x, per-block partial sums of r into partial[blockIdx]
+__global__ void __launch_bounds__(kNormBlock) normalize_partial_kernel(const double* __restrict__ z,
+                                                                      double* __restrict__ x,
+                                                                      double* __restrict__ partial,
+                                                                      int64_t n, double inv_root) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = pow(z[i], inv_root);
+    x[i] = r;
+    s += r;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// every block sums all partials in the same order, then scales its slice
+__global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __restrict__ x,
+                                                                    const double* __restrict__ partial,
+                                                                    int nparts, int64_t n) {
+  __shared__ double tot;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int j = threadIdx.x; j < nparts; j += 32) s += partial[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) tot = s;
+  }
+  __syncthreads();
+  const double t = tot;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = x[i] / t;
+}
+
+// ------------------------------------------------------------- launchers
+EdgeKernelEntry edge_entry(int N) {
+  switch (N) {
+#define STTSV_CASE(n) \
+  case n:             \
+    return edge_entry_##n();
+    STTSV_COMPILED_RANKS(STTSV_CASE)
+#undef STTSV_CASE
+    default:
+      return edge_entry_0();
+  }
+}
+
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int T, int H) {
+  return e.ring_bytes + (size_t)(T * e.block + H) * sizeof(double);
+}
+
+cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm) {
+  cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(max_blocks_per_sm, e.fn, e.block, smem);
+}
+
+cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
+                               cudaStream_t s) {
+  void* args[] = {const_cast<EdgeKernelParams*>(&p)};
+  return cudaLaunchKernel(e.fn, dim3(grid), dim3(e.block), args, smem, s);
+}
+
+static int grid_for(int64_t n, int block, int cap) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, int64_t n_active, cudaStream_t s) {
+  if (n_active <= 0) return cudaSuccess;
+  gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s) {
+  if (n_active <= 0) return cudaSuccess;
+  expand_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(ya, act, y, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_const(double* y, int64_t n, double v, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  fill_kernel<<<grid_for(n, 256, 8192), 256, 0, s>>>(y, n, v);
+  return cudaGetLastError();
+}
+
+// x and z are n_active long; `partial` holds kNormalizeScratch doubles.
+cudaError_t launch_normalize(const double* z, double* x, double* partial, int64_t n_active, int N,
+                             cudaStream_t s) {
+  if (n_active <= 0) return cudaSuccess;
+  const int grid = grid_for(n_active, kNormBlock, kNormMaxGrid);
+  normalize_partial_kernel<<<grid, kNormBlock, 0, s>>>(z, x, partial, n_active, 1.0 / double(N - 1));
+  normalize_apply_kernel<<<grid, kNormBlock, 0, s>>>(x, partial, grid, n_active);
+  return cudaGetLastError();
+}
+
+}  // namespace sttsv

@@ -1,0 +1,662 @@
+// plan.cpp — host planner and C ABI of libsttsv.so (include/sttsv.h).
+//
+// sttsv_plan_create validates the IOU hyperedges,
+// computes global degrees, relabels active vertices by descending degree
+// (hot vertices get small ids, which the kernel's scatter tiers key on),
+// buckets the edges of this shard by cardinality into SoA int32 id columns,
+// folds the per-size constant (N-1)!/|beta(k)| = (N-1)!/(k! S(N,k))
+// (PAPER.md:342 footnote, Alg. 2 factor PAPER.md:391) into the fp64 weights,
+// and uploads everything once.  sttsv_apply is then gather -> edge kernel ->
+// (NCCL allreduce) -> expand, all on the caller's stream.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace sttsv;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static sttsv_status_t fail(sttsv_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+static sttsv_status_t cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return fail(STTSV_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+  return fail(STTSV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr, what)                         \
+  do {                                               \
+    cudaError_t e_ = (expr);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+extern "C" const char* sttsv_status_string(sttsv_status_t s) {
+  switch (s) {
+    case STTSV_OK: return "STTSV_OK";
+    case STTSV_ERR_INVALID_ARGUMENT: return "STTSV_ERR_INVALID_ARGUMENT";
+    case STTSV_ERR_EDGE_SIZE: return "STTSV_ERR_EDGE_SIZE";
+    case STTSV_ERR_VERTEX_RANGE: return "STTSV_ERR_VERTEX_RANGE";
+    case STTSV_ERR_UNSORTED: return "STTSV_ERR_UNSORTED";
+    case STTSV_ERR_REPEATED_VERTEX: return "STTSV_ERR_REPEATED_VERTEX";
+    case STTSV_ERR_NONFINITE: return "STTSV_ERR_NONFINITE";
+    case STTSV_ERR_ALIAS: return "STTSV_ERR_ALIAS";
+    case STTSV_ERR_CUDA: return "STTSV_ERR_CUDA";
+    case STTSV_ERR_NCCL: return "STTSV_ERR_NCCL";
+    case STTSV_ERR_OUT_OF_MEMORY: return "STTSV_ERR_OUT_OF_MEMORY";
+    case STTSV_ERR_UNSUPPORTED: return "STTSV_ERR_UNSUPPORTED";
+  }
+  return "STTSV_ERR_UNKNOWN";
+}
+
+extern "C" const char* sttsv_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char* sttsv_version(void) { return "sttsv-b200 0.1 (sm_100a)"; }
+
+// -------------------------------------------------------------------- NCCL
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString) api.h = h;
+  });
+  return api.h ? &api : nullptr;
+}
+
+struct sttsv_comm_s {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, device = 0;
+};
+
+extern "C" sttsv_status_t sttsv_comm_unique_id(unsigned char id[128]) {
+  if (!id) return fail(STTSV_ERR_INVALID_ARGUMENT, "id is NULL");
+  NcclApi* api = nccl_api();
+  if (!api) return fail(STTSV_ERR_NCCL, "could not load libnccl.so.2");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId uid;
+  ncclResult_t r = api->GetUniqueId(&uid);
+  if (r != ncclSuccess) return fail(STTSV_ERR_NCCL, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  memcpy(id, &uid, 128);
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_comm_create(sttsv_comm_t* out, const unsigned char id[128], int world, int rank,
+                                            int device) {
+  if (!out || !id) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(STTSV_ERR_INVALID_ARGUMENT, "bad world/rank");
+  NcclApi* api = nccl_api();
+  if (!api) return fail(STTSV_ERR_NCCL, "could not load libnccl.so.2");
+  CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  auto* c = new sttsv_comm_s();
+  ncclResult_t r = api->CommInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(STTSV_ERR_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
+  }
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  *out = c;
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_comm_destroy(sttsv_comm_t c) {
+  if (!c) return STTSV_OK;
+  NcclApi* api = nccl_api();
+  if (api && c->comm) api->CommDestroy(c->comm);
+  delete c;
+  return STTSV_OK;
+}
+
+// ------------------------------------------------------------ combinatorics
+// (N-1)!/(k! S(N,k)) in long double.  S(N,k) by the explicit alternating sum
+// S(N,k) = (1/k!) sum_j (-1)^j C(k,j) (k-j)^N is exact in 128-bit integers for
+// N <= 26; beyond that the recurrence S(n,k) = k S(n-1,k) + S(n-1,k-1) in long
+// double.  |beta(k)| = k! S(N,k) = sum_j (-1)^j C(k,j) (k-j)^N  (surjections).
+static long double surjections_ld(int N, int k) {
+  if (N <= 26) {
+    __int128 tot = 0, binom = 1;
+    for (int j = 0; j <= k; ++j) {
+      __int128 p = 1;
+      for (int t = 0; t < N; ++t) p *= (k - j);
+      tot += (j & 1) ? -binom * p : binom * p;
+      binom = binom * (k - j) / (j + 1);
+    }
+    return (long double)tot;
+  }
+  std::vector<std::vector<long double>> S(N + 1, std::vector<long double>(N + 1, 0.0L));
+  S[0][0] = 1.0L;
+  for (int a = 1; a <= N; ++a)
+    for (int b = 1; b <= a; ++b) S[a][b] = (long double)b * S[a - 1][b] + S[a - 1][b - 1];
+  long double f = 1.0L;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return S[N][k] * f;
+}
+
+static long double scale_constant(int N, int k) {
+  long double f = 1.0L;
+  for (int i = 2; i <= N - 1; ++i) f *= i;
+  return f / surjections_ld(N, k);
+}
+
+// FP64 FMAs of dp_edge<k, N-k+1> (SURVEY.md Appendix A closed form) plus the
+// multiplies of series generation; used for the tile order and plan info.
+static double dp_fma(int N, int k) {
+  const double D = N - k, L = D + 1;
+  double f;
+  if (k == 1) f = D;
+  else if (k == 2) f = D;
+  else if (k == 3) f = L * (L + 1) / 2 + 4 * L - 1;
+  else f = (k - 3) * L * (L + 1) + (k + 1) * L - 1;
+  return f + 2.0 * k * D;
+}
+
+// ------------------------------------------------------------------- plans
+struct sttsv_plan_s {
+  int device = 0;
+  int64_t n = 0;
+  int32_t N = 0;
+  int world = 1, rank = 0;
+  sttsv_comm_t comm = nullptr;
+  int64_t total_edges = 0, total_inc = 0, local_edges = 0, local_inc = 0;
+  int64_t n_active = 0;
+  int64_t edges_per_size[STTSV_MAX_RANK + 1] = {0};
+  // device memory
+  void* dmem = nullptr;
+  size_t dbytes = 0;
+  int32_t* d_act = nullptr;
+  double* d_xa = nullptr;
+  double* d_ya = nullptr;
+  double* d_scratch = nullptr;
+  int32_t* d_counter = nullptr;
+  // e2e staging (sttsv_apply_host)
+  double* d_xhost = nullptr;
+  double* d_yhost = nullptr;
+  cudaStream_t host_stream = nullptr;
+  // kernel
+  EdgeKernelEntry ent{};
+  EdgeKernelParams kp{};
+  int grid = 0, block = 0;
+  size_t smem = 0;
+  int64_t stream_bytes = 0;
+  double fma = 0;
+  // edge-kernel timing (sttsv_plan_profile)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  size_t events_used = 0;
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static inline int64_t bucket_lo(int64_t mk, int world, int rank) {
+  return (int64_t)((__int128)mk * rank / world);
+}
+
+// shared by the planner and sttsv_shard_edges: per edge its position in its
+// size bucket; per bucket its global count
+static void bucket_positions(int64_t m, const int32_t* sizes, int N, std::vector<int64_t>& pos,
+                             std::vector<int64_t>& count) {
+  count.assign(N + 1, 0);
+  pos.resize(m);
+  for (int64_t e = 0; e < m; ++e) pos[e] = count[sizes[e]]++;
+}
+
+extern "C" sttsv_status_t sttsv_shard_edges(int64_t m, const int32_t* sizes, int32_t N, int world, int rank,
+                                            int64_t* out_edges, int64_t* out_count) {
+  if (!out_count || (m > 0 && (!sizes || !out_edges))) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (m < 0 || N < 1 || N > STTSV_MAX_RANK || world < 1 || rank < 0 || rank >= world)
+    return fail(STTSV_ERR_INVALID_ARGUMENT, "bad m/N/world/rank");
+  for (int64_t e = 0; e < m; ++e)
+    if (sizes[e] < 1 || sizes[e] > N) return fail(STTSV_ERR_EDGE_SIZE, "edge %lld has size %d", (long long)e, sizes[e]);
+  std::vector<int64_t> pos, count;
+  bucket_positions(m, sizes, N, pos, count);
+  int64_t c = 0;
+  for (int k = 1; k <= N; ++k) {
+    const int64_t lo = bucket_lo(count[k], world, rank), hi = bucket_lo(count[k], world, rank + 1);
+    for (int64_t e = 0; e < m; ++e)
+      if (sizes[e] == k && pos[e] >= lo && pos[e] < hi) out_edges[c++] = e;
+  }
+  *out_count = c;
+  return STTSV_OK;
+}
+
+static void free_plan(sttsv_plan_s* p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  if (p->host_stream) cudaStreamSynchronize(p->host_stream);
+  cudaDeviceSynchronize();
+  for (auto& ev : p->events) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
+  if (p->dmem) cudaFree(p->dmem);
+  if (p->d_xhost) cudaFree(p->d_xhost);
+  if (p->host_stream) cudaStreamDestroy(p->host_stream);
+  delete p;
+}
+
+extern "C" sttsv_status_t sttsv_plan_destroy(sttsv_plan_t p) {
+  free_plan(p);
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_t N, int64_t m,
+                                            const int32_t* sizes, const int32_t* indices, const double* weights,
+                                            int device, int world, int rank, sttsv_comm_t comm, uint32_t flags) {
+  if (!out) return fail(STTSV_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > INT32_MAX) return fail(STTSV_ERR_INVALID_ARGUMENT, "n must be in [1, 2^31-1], got %lld", (long long)n);
+  if (N < 1 || N > STTSV_MAX_RANK)
+    return fail(STTSV_ERR_INVALID_ARGUMENT, "rank_Nk must be in [1, %d], got %d", STTSV_MAX_RANK, N);
+  if (m < 0) return fail(STTSV_ERR_INVALID_ARGUMENT, "num_edges < 0");
+  if (m > 0 && (!sizes || !indices)) return fail(STTSV_ERR_INVALID_ARGUMENT, "sizes/indices NULL");
+  if (world < 1 || rank < 0 || rank >= world) return fail(STTSV_ERR_INVALID_ARGUMENT, "bad world/rank");
+  if (comm && (comm->world != world || comm->rank != rank || comm->device != device))
+    return fail(STTSV_ERR_INVALID_ARGUMENT, "comm world/rank/device differ from the plan's");
+  if (flags & ~(uint32_t)STTSV_CANONICALIZE)
+    return fail(STTSV_ERR_UNSUPPORTED, "flags 0x%x not implemented in this build", flags & ~(uint32_t)STTSV_CANONICALIZE);
+
+  // ---- validate; offsets
+  std::vector<int64_t> off(m + 1, 0);
+  for (int64_t e = 0; e < m; ++e) {
+    if (sizes[e] < 1 || sizes[e] > N)
+      return fail(STTSV_ERR_EDGE_SIZE, "edge %lld has size %d (rank %d)", (long long)e, sizes[e], N);
+    off[e + 1] = off[e] + sizes[e];
+  }
+  const int64_t total_inc = off[m];
+  std::vector<int32_t> canon;
+  const int32_t* idx = indices;
+  if (flags & STTSV_CANONICALIZE) {
+    canon.assign(indices, indices + total_inc);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < m; ++e) std::sort(canon.begin() + off[e], canon.begin() + off[e + 1]);
+    idx = canon.data();
+  }
+  int64_t bad_e = -1;
+  int bad_kind = 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int kind = 0;
+    for (int64_t j = off[e]; j < off[e + 1]; ++j) {
+      if (idx[j] < 0 || idx[j] >= n) { kind = 1; break; }
+      if (j > off[e] && idx[j] <= idx[j - 1]) { kind = idx[j] == idx[j - 1] ? 3 : 2; break; }
+    }
+    if (kind == 0 && weights && !std::isfinite(weights[e])) kind = 4;
+    if (kind) {
+#pragma omp critical
+      if (bad_e < 0 || e < bad_e) { bad_e = e; bad_kind = kind; }
+    }
+  }
+  if (bad_e >= 0) {
+    switch (bad_kind) {
+      case 1: return fail(STTSV_ERR_VERTEX_RANGE, "edge %lld has an id outside [0, %lld)", (long long)bad_e, (long long)n);
+      case 2: return fail(STTSV_ERR_UNSORTED, "edge %lld is not strictly increasing", (long long)bad_e);
+      case 3: return fail(STTSV_ERR_REPEATED_VERTEX, "edge %lld repeats a vertex", (long long)bad_e);
+      default: return fail(STTSV_ERR_NONFINITE, "weight of edge %lld is not finite", (long long)bad_e);
+    }
+  }
+
+  auto* p = new sttsv_plan_s();
+  p->device = device;
+  p->n = n;
+  p->N = N;
+  p->world = world;
+  p->rank = rank;
+  p->comm = comm;
+  p->total_edges = m;
+  p->total_inc = total_inc;
+
+  // ---- degrees over ALL edges (identical relabel on every rank)
+  std::vector<int64_t> deg(n, 0);
+  for (int64_t j = 0; j < total_inc; ++j) deg[idx[j]]++;
+  std::vector<int32_t> act;
+  act.reserve(1024);
+  for (int64_t v = 0; v < n; ++v)
+    if (deg[v] > 0) act.push_back((int32_t)v);
+  std::stable_sort(act.begin(), act.end(), [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
+  const int64_t na = (int64_t)act.size();
+  p->n_active = na;
+  std::vector<int32_t> newid(n, -1);
+  for (int64_t i = 0; i < na; ++i) newid[act[i]] = (int32_t)i;
+  std::vector<int64_t>().swap(deg);
+
+  // ---- buckets and this shard's slices
+  std::vector<int64_t> pos, count;
+  bucket_positions(m, sizes, N, pos, count);
+  std::vector<int64_t> lo(N + 1), mk(N + 1, 0), stride(N + 1, 0);
+  for (int k = 1; k <= N; ++k) {
+    lo[k] = bucket_lo(count[k], world, rank);
+    mk[k] = bucket_lo(count[k], world, rank + 1) - lo[k];
+    stride[k] = (mk[k] + 3) & ~(int64_t)3;
+    p->edges_per_size[k] = mk[k];
+    p->local_edges += mk[k];
+    p->local_inc += mk[k] * k;
+  }
+  // pools: ids [sum_k k*stride_k] int32, w [sum_k stride_k] f64
+  std::vector<int64_t> ids_off(N + 1, 0), w_off(N + 1, 0);
+  int64_t ids_total = 0, w_total = 0;
+  for (int k = 1; k <= N; ++k) {
+    ids_off[k] = ids_total;
+    w_off[k] = w_total;
+    ids_total += (int64_t)k * stride[k];
+    w_total += stride[k];
+  }
+  std::vector<int32_t> h_ids((size_t)ids_total, 0);
+  std::vector<double> h_w((size_t)w_total, 0.0);
+  std::vector<double> Ck(N + 1, 0.0);
+  std::vector<long double> Ckl(N + 1, 0.0L);
+  for (int k = 1; k <= N; ++k) Ckl[k] = scale_constant(N, k);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    const int k = sizes[e];
+    const int64_t le = pos[e] - lo[k];
+    if (le < 0 || le >= mk[k]) continue;
+    int32_t v[STTSV_MAX_RANK];
+    for (int i = 0; i < k; ++i) v[i] = newid[idx[off[e] + i]];
+    for (int i = 1; i < k; ++i) {  // members ascending by relabelled id
+      int32_t t = v[i];
+      int j = i - 1;
+      while (j >= 0 && v[j] > t) { v[j + 1] = v[j]; --j; }
+      v[j + 1] = t;
+    }
+    int32_t* col = h_ids.data() + ids_off[k] + le;
+    for (int i = 0; i < k; ++i) col[(int64_t)i * stride[k]] = v[i];
+    const long double w = weights ? (long double)weights[e] : (long double)k;
+    h_w[w_off[k] + le] = (double)(w * Ckl[k]);
+  }
+  std::vector<int32_t>().swap(newid);
+
+  // ---- tile order: most expensive buckets first (dynamic scheduler, LPT-like)
+  int occ = 0;
+  const int T = (int)std::min<int64_t>(16, na);
+  const int H = (int)std::max<int64_t>(T, std::min<int64_t>(na, 4096));
+  p->ent = edge_entry(N);
+  const int block = p->ent.block;
+  {
+    DeviceGuard g(device);
+    cudaError_t e0 = cudaSetDevice(device);
+    if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "cudaSetDevice"); }
+    p->smem = edge_kernel_smem_bytes(p->ent, T, H);
+    e0 = edge_kernel_config(p->ent, p->smem, &occ);
+    if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "edge kernel configuration"); }
+    if (occ < 1) { free_plan(p); return fail(STTSV_ERR_CUDA, "edge kernel cannot be resident (smem %zu)", p->smem); }
+  }
+  std::vector<int> order;
+  for (int k = 1; k <= N; ++k)
+    if (mk[k] > 0) order.push_back(k);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dp_fma(N, a) > dp_fma(N, b); });
+  EdgeKernelParams& kp = p->kp;
+  kp.N = N;
+  kp.nb = (int)order.size();
+  int64_t tiles = 0;
+  double fma = 0;
+  for (int i = 0; i < kp.nb; ++i) {
+    const int k = order[i];
+    BucketDesc& b = kp.b[i];
+    b.k = k;
+    b.m = mk[k];
+    b.stride = stride[k];
+    b.tile_begin = tiles;
+    b.ids_off = ids_off[k];
+    b.w_off = w_off[k];
+    tiles += (mk[k] + block - 1) / block;
+    fma += dp_fma(N, k) * (double)mk[k];
+  }
+  kp.num_tiles = tiles;
+  kp.n_active = (int32_t)na;
+  kp.T = T;
+  kp.H = H;
+  kp.tile_edges = block;
+  p->fma = fma;
+  p->stream_bytes = ids_total * 4 + w_total * 8;
+
+  // ---- device memory: one allocation
+  DeviceGuard g(device);
+  auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t b_ids = align(ids_total * 4), b_w = align(w_total * 8), b_act = align(na * 4 + 4),
+               b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8),
+               b_cnt = align(16);
+  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_cnt;
+  cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
+  if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
+  char* base = (char*)p->dmem;
+  int32_t* d_ids = (int32_t*)base;
+  double* d_w = (double*)(base + b_ids);
+  p->d_act = (int32_t*)(base + b_ids + b_w);
+  p->d_xa = (double*)(base + b_ids + b_w + b_act);
+  p->d_ya = (double*)(base + b_ids + b_w + b_act + b_xa);
+  p->d_scratch = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya);
+  p->d_counter = (int32_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
+  if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
+  kp.ids = d_ids;
+  kp.w = d_w;
+  kp.xa = p->d_xa;
+  kp.ya = p->d_ya;
+  kp.tile_counter = p->d_counter;
+
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int64_t grid = (int64_t)sms * std::max(occ, 1);
+  if (grid > tiles) grid = std::max<int64_t>(tiles, 1);
+  p->grid = (int)grid;
+  p->block = block;
+  *out = p;
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_plan_info(sttsv_plan_t p, sttsv_plan_info_t* info) {
+  if (!p || !info) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  memset(info, 0, sizeof(*info));
+  info->n = p->n;
+  info->rank_Nk = p->N;
+  info->world = p->world;
+  info->rank = p->rank;
+  info->num_edges = p->local_edges;
+  info->incidences = p->local_inc;
+  info->total_edges = p->total_edges;
+  info->total_incidences = p->total_inc;
+  info->n_active = p->n_active;
+  for (int k = 0; k <= STTSV_MAX_RANK; ++k) info->edges_per_size[k] = p->edges_per_size[k];
+  info->device_bytes = (int64_t)p->dbytes;
+  info->stream_bytes = p->stream_bytes;
+  info->fma_per_apply = p->fma;
+  info->hot_private = p->kp.T;
+  info->hot_shared = p->kp.H;
+  info->kernel_grid = p->grid;
+  info->kernel_block = p->block;
+  return STTSV_OK;
+}
+
+extern "C" int sttsv_apply_launches(sttsv_plan_t p) {
+  if (!p) return 0;
+  int l = 0;
+  if (p->n_active > 0) l += 2;          // gather + expand
+  if (p->kp.num_tiles > 0) l += 1;      // edge kernel
+  return l;
+}
+
+extern "C" sttsv_status_t sttsv_plan_profile(sttsv_plan_t p, int enable) {
+  if (!p) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (enable) p->events_used = 0;
+  p->profiling = enable != 0;
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_plan_profile_read(sttsv_plan_t p, double* total_ms, int64_t* launches) {
+  if (!p || !total_ms || !launches) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(p->device);
+  double tot = 0.0;
+  for (size_t i = 0; i < p->events_used; ++i) {
+    CUDA_TRY(cudaEventSynchronize(p->events[i].second), "cudaEventSynchronize");
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p->events[i].first, p->events[i].second), "cudaEventElapsedTime");
+    tot += ms;
+  }
+  *total_ms = tot;
+  *launches = (int64_t)p->events_used;
+  return STTSV_OK;
+}
+
+static sttsv_status_t check_async(sttsv_plan_s* p) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
+  if (p->comm) {
+    NcclApi* api = nccl_api();
+    ncclResult_t r = ncclSuccess;
+    if (api && api->CommGetAsyncError && api->CommGetAsyncError(p->comm->comm, &r) == ncclSuccess && r != ncclSuccess)
+      return fail(STTSV_ERR_NCCL, "NCCL async error: %s", api->GetErrorString(r));
+  }
+  return STTSV_OK;
+}
+
+// y_a = (B x_a^{N-1}) on the active vertices (x_a already gathered)
+static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
+  if (p->n_active == 0) return STTSV_OK;
+  CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
+  if (p->kp.num_tiles > 0) {
+    CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int32_t), s), "memset counter");
+    std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+    if (p->profiling) {
+      if (p->events_used == p->events.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> e2;
+        CUDA_TRY(cudaEventCreate(&e2.first), "cudaEventCreate");
+        CUDA_TRY(cudaEventCreate(&e2.second), "cudaEventCreate");
+        p->events.push_back(e2);
+      }
+      ev = &p->events[p->events_used++];
+      CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
+    }
+    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s), "edge kernel launch");
+    if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
+  }
+  if (p->comm && p->world > 1) {
+    NcclApi* api = nccl_api();
+    ncclResult_t r = api->AllReduce(p->d_ya, p->d_ya, (size_t)p->n_active, ncclFloat64, ncclSum, p->comm->comm, s);
+    if (r != ncclSuccess) return fail(STTSV_ERR_NCCL, "ncclAllReduce: %s", api->GetErrorString(r));
+  }
+  return STTSV_OK;
+}
+
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+extern "C" sttsv_status_t sttsv_apply(sttsv_plan_t p, const double* x, double* y, void* stream) {
+  if (!p || !x || !y) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  const size_t bytes = (size_t)p->n * sizeof(double);
+  if (overlap(x, bytes, y, bytes)) return fail(STTSV_ERR_ALIAS, "x and y overlap");
+  DeviceGuard g(p->device);
+  sttsv_status_t st = check_async(p);
+  if (st != STTSV_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->n_active, s), "gather launch");
+  st = apply_active(p, s);
+  if (st != STTSV_OK) return st;
+  CUDA_TRY(cudaMemsetAsync(y, 0, bytes, s), "memset y");
+  CUDA_TRY(launch_expand(p->d_ya, p->d_act, y, p->n_active, s), "expand launch");
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host, double* y_host) {
+  if (!p || !x_host || !y_host) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  const size_t bytes = (size_t)p->n * sizeof(double);
+  if (overlap(x_host, bytes, y_host, bytes)) return fail(STTSV_ERR_ALIAS, "x and y overlap");
+  DeviceGuard g(p->device);
+  if (!p->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->host_stream, cudaStreamNonBlocking), "stream");
+  if (!p->d_xhost) {
+    CUDA_TRY(cudaMalloc(&p->d_xhost, 2 * bytes), "cudaMalloc e2e staging");
+    p->d_yhost = p->d_xhost + p->n;
+  }
+  cudaStream_t s = p->host_stream;
+  CUDA_TRY(cudaMemcpyAsync(p->d_xhost, x_host, bytes, cudaMemcpyHostToDevice, s), "H2D x");
+  sttsv_status_t st = sttsv_apply(p, p->d_xhost, p->d_yhost, s);
+  if (st != STTSV_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(y_host, p->d_yhost, bytes, cudaMemcpyDeviceToHost, s), "D2H y");
+  CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_power_iterate(sttsv_plan_t p, double* x, double* z, int iters, void* stream) {
+  if (!p || !x) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (iters < 0) return fail(STTSV_ERR_INVALID_ARGUMENT, "iters < 0");
+  if (p->N < 2) return fail(STTSV_ERR_INVALID_ARGUMENT, "power iteration needs rank >= 2");
+  const size_t bytes = (size_t)p->n * sizeof(double);
+  if (z && overlap(x, bytes, z, bytes)) return fail(STTSV_ERR_ALIAS, "x and z overlap");
+  if (iters == 0) return STTSV_OK;
+  DeviceGuard g(p->device);
+  sttsv_status_t st = check_async(p);
+  if (st != STTSV_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->n_active, s), "gather launch");
+  for (int it = 0; it < iters; ++it) {
+    st = apply_active(p, s);
+    if (st != STTSV_OK) return st;
+    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_scratch, p->n_active, p->N, s), "normalize launch");
+  }
+  CUDA_TRY(cudaMemsetAsync(x, 0, bytes, s), "memset x");
+  CUDA_TRY(launch_expand(p->d_xa, p->d_act, x, p->n_active, s), "expand x");
+  if (z) {
+    CUDA_TRY(cudaMemsetAsync(z, 0, bytes, s), "memset z");
+    CUDA_TRY(launch_expand(p->d_ya, p->d_act, z, p->n_active, s), "expand z");
+  }
+  return STTSV_OK;
+}

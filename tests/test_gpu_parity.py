@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance (north_star): relative L-inf  max|y_gpu - y_ora| / max|y_ora| <= 1e-11;
+the per-edge DP is subtraction-free for x > 0, so small cases are held to 1e-13.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11       # north_star parity bound
+TIGHT = 1e-13     # small, well-conditioned cases
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2311_08595_b200 as S
+    return S
+
+
+def gpu_apply(S, torch, hg, x=None, weights="hg", **kw):
+    w = hg.weights if weights == "hg" else weights
+    plan = S.Plan(hg.n, hg.rank, hg.sizes, hg.indices, w, **kw)
+    xx = torch.from_numpy(np.ascontiguousarray(hg.x if x is None else x, dtype=np.float64)).cuda()
+    y = plan.apply(xx)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), plan
+
+
+def to_hg(n, N, edges, weights, x):
+    sizes = np.array([len(e) for e in edges], dtype=np.int32)
+    off = np.zeros(len(edges) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=off[1:])
+    idx = np.array([v for e in edges for v in e], dtype=np.int32) if edges else np.zeros(0, np.int32)
+    return W.Hypergraph(n, N, sizes, off, idx, np.asarray(weights, dtype=np.float64), np.asarray(x, dtype=np.float64))
+
+
+# ------------------------------------------------------------------ pins
+def test_fig1(S, torch_cuda):
+    hg = W.fig1()
+    y, _ = gpu_apply(S, torch_cuda, hg, x=np.ones(8))
+    assert rel(y, [3, 2, 3, 4, 2, 3, 3, 1]) < TIGHT           # PAPER.md:343 degree identity
+    x = np.arange(1, 9, dtype=np.float64)
+    for w in (hg.sizes.astype(np.float64), np.ones(6)):
+        y, _ = gpu_apply(S, torch_cuda, hg, x=x, weights=w)
+        assert rel(y, oracle.sttsv(hg, x=x, weights=w)) < TIGHT
+    y, _ = gpu_apply(S, torch_cuda, hg, x=x, weights=None)     # NULL weights => w = |e|
+    assert rel(y, [192, 108, 96, 585 / 2, 397, 169, 2393 / 7, 6]) < TIGHT
+
+
+@pytest.mark.parametrize("N", [2, 3, 5, 8, 10, 12, 16, 25, 17, 20, 32])
+def test_every_bucket_single_edges(S, torch_cuda, N):
+    """One edge of every size k = 1..N (P13-style x_i = 1/(i+2)), each bucket's DP alone."""
+    edges, xs = [], []
+    for k in range(1, N + 1):
+        base = len(xs)
+        edges.append(list(range(base, base + k)))
+        xs.extend(1.0 / (i + 2) for i in range(k))
+    hg = to_hg(len(xs), N, edges, np.linspace(0.5, 1.5, len(edges)), xs)
+    y, _ = gpu_apply(S, torch_cuda, hg)
+    ref = oracle.sttsv(hg)
+    for e in range(len(edges)):
+        ids = edges[e]
+        assert rel(y[ids], ref[ids]) < TIGHT, (N, len(ids))
+
+
+@pytest.mark.parametrize("N", [4, 8, 12, 25, 19])
+def test_random_buckets_ragged(S, torch_cuda, N):
+    """Several tiles per bucket plus a ragged tail, random x in (0, 1]."""
+    rng = np.random.default_rng(N)
+    n = 3000
+    edges = []
+    for k in range(1, N + 1):
+        cnt = 600 + 37 * k if N <= 12 else 40 + k
+        for _ in range(cnt):
+            edges.append(sorted(rng.choice(n, size=k, replace=False).tolist()))
+    rng.shuffle(edges)
+    hg = to_hg(n, N, edges, rng.uniform(0.1, 2.0, len(edges)), rng.uniform(0.01, 1.0, n))
+    y, _ = gpu_apply(S, torch_cuda, hg)
+    assert rel(y, oracle.sttsv(hg)) < TIGHT
+
+
+# -------------------------------------------------------- config shapes
+@pytest.mark.parametrize("name,m,n", [
+    ("tiny", None, None),
+    ("mid", 200_000, None),
+    ("high-rank", 600, None),
+    ("large", 300_000, None),
+    ("centrality", 100_000, None),
+])
+def test_configs_reduced(S, torch_cuda, name, m, n):
+    hg = W.generate(name, m=m, n=n)
+    y, plan = gpu_apply(S, torch_cuda, hg)
+    assert rel(y, oracle.sttsv(hg)) < TOL
+    if name == "tiny":
+        assert rel(y, oracle.sttsv(hg, mode="literal")) < TOL
+    info = plan.info()
+    assert info["total_incidences"] == hg.incidences and info["num_edges"] == hg.m
+
+
+def test_tiny_degree_identity(S, torch_cuda):
+    hg = W.generate("tiny")
+    y, _ = gpu_apply(S, torch_cuda, hg, x=np.ones(hg.n), weights=None)
+    d = np.bincount(hg.indices, minlength=hg.n).astype(np.float64)
+    assert rel(y, d) < TIGHT
+
+
+def test_power_iteration_centrality_reduced(S, torch_cuda):
+    torch = torch_cuda
+    hg = W.generate("centrality", m=60_000)
+    iters = 50
+    xo, zo = oracle.power_iteration(hg, iters)
+    plan = S.Plan.from_hypergraph(hg)
+    x = torch.full((hg.n,), 1.0 / hg.n, dtype=torch.float64, device="cuda")
+    x, z = plan.power_iterate(x, iters)
+    torch.cuda.synchronize()
+    assert rel(x.cpu().numpy(), xo) < TOL
+    assert rel(z.cpu().numpy(), zo) < TOL
+    assert abs(x.sum().item() - 1.0) < 1e-12
+
+
+def test_power_iteration_pins(S, torch_cuda):
+    torch = torch_cuda
+    plan = S.Plan(2, 2, np.array([2], np.int32), np.array([0, 1], np.int32), np.array([2.0]))
+    x = torch.tensor([0.3, 0.7], dtype=torch.float64, device="cuda")
+    x, z = plan.power_iterate(x, 3)
+    assert np.allclose(x.cpu().numpy(), 0.5, atol=1e-15) and np.allclose(z.cpu().numpy(), 0.5, atol=1e-15)
+    edges = [list(c) for c in itertools.combinations(range(6), 3)]
+    hg = to_hg(6, 3, edges, [3.0] * len(edges), np.zeros(6))
+    plan = S.Plan.from_hypergraph(hg)
+    x = torch.rand(6, dtype=torch.float64, device="cuda") + 0.1
+    x, _ = plan.power_iterate(x, 60)
+    assert np.allclose(x.cpu().numpy(), 1 / 6, atol=1e-12)
+
+
+# -------------------------------------------------------- edge cases
+def test_edge_cases(S, torch_cuda):
+    torch = torch_cuda
+    # no edges: y = 0
+    plan = S.Plan(5, 3, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    y = plan.apply(torch.ones(5, dtype=torch.float64, device="cuda"))
+    assert torch.count_nonzero(y).item() == 0
+    # N = 1, singletons: s_v = sum of weights of {v}
+    hg = to_hg(4, 1, [[0], [2], [2]], [1.5, 2.0, 0.25], [3.0, 1.0, 7.0, 1.0])
+    y, _ = gpu_apply(S, torch, hg)
+    assert np.allclose(y, [1.5, 0, 2.25, 0], rtol=0, atol=1e-15)
+    # singletons at higher rank, duplicates, rank above max |e|, isolated vertices, zero x entries
+    rng = np.random.default_rng(5)
+    edges = [[0], [1, 2], [1, 2], [0, 3, 5], [2, 3, 4, 5], [7]]
+    x = np.array([0.0, 0.5, 1.25, 0.75, 0.0, 1.0, 9.0, 0.3])
+    hg = to_hg(9, 7, edges, rng.uniform(0.5, 1.5, len(edges)), np.append(x, 0.0))
+    y, _ = gpu_apply(S, torch, hg)
+    ref = oracle.sttsv(hg)
+    assert rel(y, ref) < TIGHT and y[6] == 0.0 and y[8] == 0.0
+    # negative x (the identity is polynomial): still matches the oracle
+    hg2 = W.generate("tiny")
+    xneg = hg2.x - 0.5
+    y, _ = gpu_apply(S, torch, hg2, x=xneg)
+    assert rel(y, oracle.sttsv(hg2, x=xneg)) < 1e-11
+    # canonicalize flag sorts unsorted edges
+    plan = S.Plan(6, 3, np.array([3], np.int32), np.array([4, 0, 2], np.int32), flags=S.STTSV_CANONICALIZE)
+    xx = torch.arange(1, 7, dtype=torch.float64, device="cuda")
+    y = plan.apply(xx).cpu().numpy()
+    ref = oracle.sttsv(to_hg(6, 3, [[0, 2, 4]], [3.0], np.arange(1, 7.0)))
+    assert rel(y, ref) < TIGHT
+    # aliasing x and y is refused
+    with pytest.raises(S.SttsvError) as ei:
+        plan.apply(xx, xx)
+    assert ei.value.name == "STTSV_ERR_ALIAS"
+
+
+def test_fake_shards_sum(S, torch_cuda):
+    """world = 3 plans on one GPU (comm = NULL => each returns its partial sum)."""
+    torch = torch_cuda
+    hg = W.generate("mid", m=50_000)
+    x = torch.from_numpy(hg.x).cuda()
+    tot = torch.zeros_like(x)
+    for r in range(3):
+        plan = S.Plan.from_hypergraph(hg, world=3, rank=r)
+        tot += plan.apply(x)
+    assert rel(tot.cpu().numpy(), oracle.sttsv(hg)) < TOL
+
+
+def test_nccl_world1(S, torch_cuda):
+    torch = torch_cuda
+    hg = W.generate("mid", m=20_000)
+    uid = S.sttsv_comm_unique_id()
+    comm = S.sttsv_comm_create(uid, 1, 0, 0)
+    try:
+        plan = S.Plan.from_hypergraph(hg, comm=comm)
+        y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
+        assert rel(y, oracle.sttsv(hg)) < TOL
+        plan.close()
+    finally:
+        S.sttsv_comm_destroy(comm)
+
+
+def test_apply_host_matches_device(S, torch_cuda):
+    hg = W.generate("large", m=100_000, n=1_000_000)
+    y, plan = gpu_apply(S, torch_cuda, hg)
+    yh = plan.apply_host(hg.x)
+    assert rel(yh, y) < 1e-14
+    assert rel(yh, oracle.sttsv(hg)) < TOL
+
+
+# ------------------------------------------- full BASELINE sizes (bench launch config)
+@pytest.mark.parametrize("name", ["mid", "high-rank", "centrality", "large"])
+def test_full_size_sampled(S, torch_cuda, name):
+    """Full config sizes, the kernel configuration bench.py times: sampled
+    cold vertices one by one against the oracle, and the degree identity
+    (x = 1, w = |e|) over every vertex (a property that holds at any size)."""
+    torch = torch_cuda
+    hg = W.generate(name)
+    y, plan = gpu_apply(S, torch, hg)
+    deg = np.bincount(hg.indices, minlength=hg.n)
+    rng = np.random.default_rng(0)
+    cand = np.where((deg > 0) & (deg <= 3))[0]
+    verts = np.concatenate([rng.choice(cand, size=min(12, len(cand)), replace=False),
+                            np.where(deg == 0)[0][:3]])
+    ref = oracle.sttsv_vertices(hg, verts)
+    for v, r in zip(verts, ref):
+        assert abs(y[v] - r) <= 1e-12 * max(abs(r), 1e-300) or (r == 0 and y[v] == 0), (v, y[v], r)
+    plan.close()
+    del plan
+    y1, plan = gpu_apply(S, torch, hg, x=np.ones(hg.n), weights=None)
+    assert rel(y1, deg.astype(np.float64)) < TOL
