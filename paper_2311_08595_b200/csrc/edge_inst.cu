@@ -14,7 +14,8 @@ namespace sttsv {
 EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   EdgeKernelEntry e;
   e.fn = (const void*)edge_kernel<STTSV_INST_N>;
-  e.block = EdgeCfg<STTSV_INST_N>::BLOCK;
+  e.block = EdgeCfg<STTSV_INST_N>::THREADS;
+  e.tile = EdgeCfg<STTSV_INST_N>::TILE;
   e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::STAGES * EdgeCfg<STTSV_INST_N>::STAGE_BYTES;
   e.rank = STTSV_INST_N;
   return e;

@@ -1,22 +1,28 @@
 // edge_kernel.cuh — the hot kernel of one STTSV apply.
 //
-// Persistent CTAs claim tiles of TILE edges from a device counter.  A tile
-// lies in one cardinality bucket (size k), so the switch on k is uniform over
-// the CTA and every (k, L = N-k+1) runs the fully unrolled register DP of
-// dp.cuh, one edge per thread.  The tile's SoA id columns and weights are
-// staged into shared memory by 1-D TMA bulk copies (cp.async.bulk, SASS
-// UBLKCP) on an STAGES-deep mbarrier ring, so the HBM stream runs ahead of the
-// FP64 work independently of occupancy.
+// Work decomposition.  The plan stores each cardinality bucket k as SoA int32
+// id columns + fp64 weights w' = w (N-1)!/|beta(k)| (PAPER.md:342 footnote and
+// Alg. 2's factor), edges sorted lexicographically by their
+// (degree-relabelled, ascending) member ids.  A tile is TILE = 32*NCW
+// consecutive edges of one bucket; tiles are ordered most-expensive bucket
+// first and dealt to the persistent CTAs round-robin.
 //
-// Each contribution delta = w' c (w' = w (N-1)!/|beta(k)| folded at plan time,
-// PAPER.md:391) is reduced through four tiers keyed on the relabelled vertex
-// id (ids are ordered by descending degree, so hot vertices are small):
-//   0. edge slot i holds vertex i (i < kDiag)  -> register accumulator racc[i]
-//   1. id < T                                   -> this thread's private shared
-//      column pc[id][tid] (plain read-modify-write: no atomics, no conflicts)
-//   2. T <= id < H                              -> CTA shared accumulator (atomicAdd)
-//   3. id >= H                                  -> red.global.add.f64 into y_a
-// Each CTA flushes tiers 0-2 into y_a once, after its last tile.
+// Warp specialisation.  Per CTA, one producer warp streams tiles into an
+// STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk ->
+// SASS UBLKCP, completion on a `full` mbarrier with expect_tx); NCW consumer
+// warps each take 32 edges of the tile (one edge per lane), run the fully
+// unrolled register DP of dp.cuh for (k, L = N-k+1), and release the stage on
+// an `empty` mbarrier.  No CTA-wide barrier sits on the tile loop.
+//
+// Scatter.  Because edges are sorted, the 32 lanes of a warp mostly hold the
+// SAME vertex in a given slot (the hottest vertices sit in the low slots).
+// For each slot the warp reduces its 32 contributions over runs of equal
+// adjacent ids (a shuffle butterfly when the whole warp is one run, else a
+// segmented suffix scan), and only each run's head lane deposits:
+//   slot i holds vertex i (i < kDiag)  -> register accumulator racc[i]
+//   id < H                             -> CTA shared accumulator sacc (atomicAdd)
+//   id >= H                            -> red.global.add.f64 into y_a
+// Each CTA flushes racc and sacc into y_a once, after its last tile.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,14 +34,17 @@
 namespace sttsv {
 
 constexpr int kDiag = 8;
+constexpr unsigned kFull = 0xffffffffu;
 
 template <int N>
 struct EdgeCfg {
-  static constexpr int BLOCK = (N >= 1 && N <= 16) ? 256 : 128;  // = TILE (one edge per thread)
+  static constexpr int NCW = (N >= 1 && N <= 16) ? 8 : 4;  // consumer warps
+  static constexpr int TILE = 32 * NCW;                    // edges per tile
+  static constexpr int THREADS = TILE + 32;                // + one producer warp
   static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
-  static constexpr int STAGES = N <= 8 ? 4 : 3;
+  static constexpr int STAGES = 4;
   static constexpr int MIN_BLOCKS = 2;
-  static constexpr int STAGE_BYTES = BLOCK * (4 * KMAX + 8);
+  static constexpr int STAGE_BYTES = TILE * (4 * KMAX + 8);
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -58,6 +67,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -67,17 +79,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// ------------------------------------------------------------ scatter tiers
-template <int BLOCK>
-__device__ __forceinline__ void deposit(int i, int v, double d, double (&racc)[kDiag], double* __restrict__ pc,
-                                        double* __restrict__ sacc, double* __restrict__ ya, int T, int H,
-                                        int tid) {
-  if (i < kDiag && v == i) {
+// ------------------------------------------------------------ scatter
+__device__ __forceinline__ void deposit_run(int slot, int v, double d, double (&racc)[kDiag],
+                                            double* __restrict__ sacc, double* __restrict__ ya, int H) {
+  if (slot < kDiag && v == slot) {
 #pragma unroll
     for (int q = 0; q < kDiag; ++q)
-      if (q == i) racc[q] += d;
-  } else if (v < T) {
-    pc[v * BLOCK + tid] += d;
+      if (q == slot) racc[q] += d;
   } else if (v < H) {
     atomicAdd(&sacc[v], d);
   } else {
@@ -85,34 +93,62 @@ __device__ __forceinline__ void deposit(int i, int v, double d, double (&racc)[k
   }
 }
 
-// one edge of a size-K bucket, ids/w from the shared stage
-template <int N, int K, int BLOCK>
-__device__ __forceinline__ void edge_from_stage(const int32_t* __restrict__ sids, const double* __restrict__ sw,
-                                                const double* __restrict__ xa, double (&racc)[kDiag],
-                                                double* pc, double* sacc, double* ya, int T, int H, int tid) {
+// Reduce (v, d) over the warp's runs of equal adjacent v; each run's first
+// lane deposits the run total.  v < 0 marks an empty lane (ragged tail).
+__device__ __forceinline__ void warp_deposit(int slot, int v, double d, int lane, double (&racc)[kDiag],
+                                             double* __restrict__ sacc, double* __restrict__ ya, int H) {
+  const int v0 = __shfl_sync(kFull, v, 0);
+  if (__all_sync(kFull, v == v0)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
+    if (lane == 0 && v >= 0) deposit_run(slot, v, d, racc, sacc, ya, H);
+    return;
+  }
+  // segmented suffix scan: after the loop a lane holds the sum from itself to
+  // the end of its run (f = "my run ends inside the span summed so far")
+  const int vn = __shfl_down_sync(kFull, v, 1);
+  int f = (lane == 31) || (vn != v);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double dn = __shfl_down_sync(kFull, d, o);
+    const int fn = __shfl_down_sync(kFull, f, o);
+    if (!f && lane + o < 32) {
+      d += dn;
+      f = fn;
+    }
+  }
+  const int vp = __shfl_up_sync(kFull, v, 1);
+  if ((lane == 0 || vp != v) && v >= 0) deposit_run(slot, v, d, racc, sacc, ya, H);
+}
+
+// 32 edges of a size-K bucket, one per lane, from the shared stage
+template <int N, int K, int TILE>
+__device__ __forceinline__ void warp_edges(const int32_t* __restrict__ sids, const double* __restrict__ sw,
+                                           int col, bool valid, const double* __restrict__ xa,
+                                           double (&racc)[kDiag], double* sacc, double* ya, int H, int lane) {
   constexpr int L = N - K + 1;
   int id[K];
   double x[K], c[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) id[i] = sids[i * BLOCK + tid];
+  for (int i = 0; i < K; ++i) id[i] = valid ? sids[i * TILE + col] : -1;
 #pragma unroll
-  for (int i = 0; i < K; ++i) x[i] = __ldg(xa + id[i]);
-  const double w = sw[tid];
+  for (int i = 0; i < K; ++i) x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+  const double w = valid ? sw[col] : 0.0;
   dp_edge<K, L>(x, c);
 #pragma unroll
-  for (int i = 0; i < K; ++i) deposit<BLOCK>(i, id[i], w * c[i], racc, pc, sacc, ya, T, H, tid);
+  for (int i = 0; i < K; ++i) warp_deposit(i, id[i], w * c[i], lane, racc, sacc, ya, H);
 }
 
-template <int N, int K, int BLOCK>
-__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, const double* xa,
-                                           double (&racc)[kDiag], double* pc, double* sacc, double* ya, int T,
-                                           int H, int tid) {
+template <int N, int K, int TILE>
+__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int col, bool valid,
+                                           const double* xa, double (&racc)[kDiag], double* sacc, double* ya,
+                                           int H, int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      edge_from_stage<N, K, BLOCK>(sids, sw, xa, racc, pc, sacc, ya, T, H, tid);
+      warp_edges<N, K, TILE>(sids, sw, col, valid, xa, racc, sacc, ya, H, lane);
       return;
     }
-    dispatch_k<N, K + 1, BLOCK>(k, sids, sw, xa, racc, pc, sacc, ya, T, H, tid);
+    dispatch_k<N, K + 1, TILE>(k, sids, sw, col, valid, xa, racc, sacc, ya, H, lane);
   }
 }
 
@@ -182,110 +218,107 @@ static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* 
 }
 
 
-template <int BLOCK>
-__device__ __forceinline__ void edge_generic_from_stage(int N, int k, const int32_t* sids, const double* sw,
-                                                        const double* xa, double (&racc)[kDiag], double* pc,
-                                                        double* sacc, double* ya, int T, int H, int tid) {
+template <int TILE>
+__device__ __forceinline__ void warp_edges_generic(int N, int k, const int32_t* sids, const double* sw, int col,
+                                                   bool valid, const double* xa, double (&racc)[kDiag],
+                                                   double* sacc, double* ya, int H, int lane) {
+  int id[STTSV_MAX_RANK];
   double x[STTSV_MAX_RANK], c[STTSV_MAX_RANK];
-  for (int i = 0; i < k; ++i) x[i] = __ldg(xa + sids[i * BLOCK + tid]);
+  for (int i = 0; i < k; ++i) {
+    id[i] = valid ? sids[i * TILE + col] : -1;
+    x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+  }
   dp_edge_generic(k, N - k + 1, x, c);
-  const double w = sw[tid];
-  for (int i = 0; i < k; ++i) deposit<BLOCK>(i, sids[i * BLOCK + tid], w * c[i], racc, pc, sacc, ya, T, H, tid);
+  const double w = valid ? sw[col] : 0.0;
+  for (int i = 0; i < k; ++i) warp_deposit(i, id[i], w * c[i], lane, racc, sacc, ya, H);
 }
 
 // ------------------------------------------------------------- the kernel
 // N == 0 is the generic instantiation (any rank <= STTSV_MAX_RANK).
 template <int N>
-__global__ void __launch_bounds__(EdgeCfg<N>::BLOCK, EdgeCfg<N>::MIN_BLOCKS)
+__global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     edge_kernel(const __grid_constant__ EdgeKernelParams p) {
   using Cfg = EdgeCfg<N>;
-  constexpr int BLOCK = Cfg::BLOCK, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX;
+  constexpr int TILE = Cfg::TILE, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX, NCW = Cfg::NCW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // layout: [STAGES][ ids KMAX*BLOCK int32 | w BLOCK f64 ] | pc [T][BLOCK] f64 | sacc [H] f64
+  // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ] | sacc [H] f64
   unsigned char* ring = smem_raw;
-  double* pc = reinterpret_cast<double*>(smem_raw + STAGES * Cfg::STAGE_BYTES);
-  double* sacc = pc + p.T * BLOCK;
-  __shared__ uint64_t full[STAGES];
-  __shared__ int64_t s_tile[STAGES];
-  __shared__ int s_bucket[STAGES];
-  const int tid = threadIdx.x;
+  double* sacc = reinterpret_cast<double*>(smem_raw + STAGES * Cfg::STAGE_BYTES);
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t G = gridDim.x;
 
-  for (int j = tid; j < p.T * BLOCK + p.H; j += BLOCK) pc[j] = 0.0;
-  double racc[kDiag];
-#pragma unroll
-  for (int i = 0; i < kDiag; ++i) racc[i] = 0.0;
-
-  // producer: claim the next tile and start its copies into stage s
-  auto produce = [&](int s) {
-    const int64_t tile = atomicAdd(p.tile_counter, 1);
-    s_tile[s] = tile;
-    if (tile >= p.num_tiles) return;
-    int b = 0;
-    while (b + 1 < p.nb && tile >= p.b[b + 1].tile_begin) ++b;
-    s_bucket[s] = b;
-    const BucketDesc& bd = p.b[b];
-    const int64_t e0 = (tile - bd.tile_begin) * BLOCK;
-    const int64_t cnt = bd.m - e0 < BLOCK ? bd.m - e0 : BLOCK;
-    const uint32_t id_bytes = (uint32_t)(((cnt + 3) & ~3LL) * 4);
-    const uint32_t w_bytes = (uint32_t)(((cnt + 1) & ~1LL) * 8);
-    unsigned char* st = ring + s * Cfg::STAGE_BYTES;
-    mbar_arrive_expect_tx(&full[s], id_bytes * bd.k + w_bytes);
-    for (int i = 0; i < bd.k; ++i)
-      bulk_g2s(st + i * BLOCK * 4, p.ids + bd.ids_off + i * bd.stride + e0, id_bytes, &full[s]);
-    bulk_g2s(st + KMAX * BLOCK * 4, p.w + bd.w_off + e0, w_bytes, &full[s]);
-  };
-
+  for (int j = tid; j < p.H; j += Cfg::THREADS) sacc[j] = 0.0;
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
     fence_proxy_async();
-    for (int s = 0; s < STAGES; ++s) produce(s);
   }
   __syncthreads();
 
-  for (int it = 0;; ++it) {
-    const int s = it % STAGES;
-    const int64_t tile = s_tile[s];
-    if (tile >= p.num_tiles) break;
-    const BucketDesc& bd = p.b[s_bucket[s]];
-    mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
-    const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
-    const int32_t* sids = reinterpret_cast<const int32_t*>(st);
-    const double* sw = reinterpret_cast<const double*>(st + KMAX * BLOCK * 4);
-    const int64_t e = (tile - bd.tile_begin) * BLOCK + tid;
-    if (e < bd.m) {
-      if constexpr (N > 0) {
-        dispatch_k<N, 1, BLOCK>(bd.k, sids, sw, p.xa, racc, pc, sacc, p.ya, p.T, p.H, tid);
-      } else {
-        edge_generic_from_stage<BLOCK>(p.N, bd.k, sids, sw, p.xa, racc, pc, sacc, p.ya, p.T, p.H, tid);
+  if (warp == NCW) {
+    // ---------------- producer warp: TMA bulk copies of tile t into stage it % STAGES
+    if (lane == 0) {
+      int64_t it = 0;
+      for (int64_t t = blockIdx.x; t < p.num_tiles; t += G, ++it) {
+        const int s = (int)(it % STAGES);
+        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+        int b = 0;
+        while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
+        const BucketDesc& bd = p.b[b];
+        const int64_t e0 = (t - bd.tile_begin) * TILE;
+        const int64_t cnt = bd.m - e0 < TILE ? bd.m - e0 : TILE;
+        const uint32_t id_bytes = (uint32_t)(((cnt + 3) & ~3LL) * 4);
+        const uint32_t w_bytes = (uint32_t)(((cnt + 1) & ~1LL) * 8);
+        unsigned char* st = ring + s * Cfg::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], id_bytes * bd.k + w_bytes);
+        for (int i = 0; i < bd.k; ++i)
+          bulk_g2s(st + i * TILE * 4, p.ids + bd.ids_off + i * bd.stride + e0, id_bytes, &full[s]);
+        bulk_g2s(st + KMAX * TILE * 4, p.w + bd.w_off + e0, w_bytes, &full[s]);
       }
     }
-    __syncthreads();  // stage s fully consumed
-    if (tid == 0) {
-      fence_proxy_async();
-      produce(s);
+  } else {
+    // ---------------- consumer warps
+    double racc[kDiag];
+#pragma unroll
+    for (int i = 0; i < kDiag; ++i) racc[i] = 0.0;
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < p.num_tiles; t += G, ++it) {
+      const int s = (int)(it % STAGES);
+      int b = 0;
+      while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
+      const BucketDesc& bd = p.b[b];
+      const int64_t e0 = (t - bd.tile_begin) * TILE + warp * 32;
+      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      if (e0 < bd.m) {
+        const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
+        const int32_t* sids = reinterpret_cast<const int32_t*>(st);
+        const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
+        const bool valid = e0 + lane < bd.m;
+        const int col = warp * 32 + lane;
+        if constexpr (N > 0) {
+          dispatch_k<N, 1, TILE>(bd.k, sids, sw, col, valid, p.xa, racc, sacc, p.ya, p.H, lane);
+        } else {
+          warp_edges_generic<TILE>(p.N, bd.k, sids, sw, col, valid, p.xa, racc, sacc, p.ya, p.H, lane);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // fold the register accumulators (vertex i < kDiag exists whenever racc[i] != 0, and H >= min(n_a, kDiag))
+#pragma unroll
+    for (int i = 0; i < kDiag; ++i) {
+      double v = racc[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if (lane == 0 && v != 0.0) atomicAdd(&sacc[i], v);
     }
   }
-
-  // flush tier 0 into the private columns (racc[i] != 0 only if vertex i exists, and i < kDiag <= T then)
-#pragma unroll
-  for (int i = 0; i < kDiag; ++i)
-    if (racc[i] != 0.0) pc[i * BLOCK + tid] += racc[i];
   __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int t = warp; t < p.T; t += BLOCK / 32) {
-    double sum = 0.0;
-    for (int j = lane; j < BLOCK; j += 32) sum += pc[t * BLOCK + j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0 && sum != 0.0) atomicAdd(&p.ya[t], sum);
-  }
-  for (int j = p.T + tid; j < p.H; j += BLOCK)
+  for (int j = tid; j < p.H; j += Cfg::THREADS)
     if (sacc[j] != 0.0) atomicAdd(&p.ya[j], sacc[j]);
-}
-
-template <int N>
-constexpr size_t edge_kernel_smem(int T, int H) {
-  return (size_t)EdgeCfg<N>::STAGES * EdgeCfg<N>::STAGE_BYTES + (size_t)(T * EdgeCfg<N>::BLOCK + H) * 8;
 }
 
 }  // namespace sttsv

@@ -33,11 +33,10 @@ struct EdgeKernelParams {
   const double* xa;      // x on active vertices (relabelled)
   double* ya;            // y on active vertices (accumulated)
   int32_t n_active;
-  int32_t T;             // ids < T: thread-private accumulation slots
+  int32_t T;             // register-accumulated slots (slot i holding vertex i, i < T)
   int32_t H;             // ids < H: CTA shared-memory accumulators
-  int32_t tile_edges;    // edges per tile (= blockDim.x)
-  int64_t num_tiles;
-  int32_t* tile_counter; // dynamic tile scheduler (zeroed before each launch)
+  int32_t tile_edges;    // edges per tile
+  int64_t num_tiles;     // tiles are dealt round-robin to the persistent CTAs
 };
 
 // Ranks with a fully unrolled edge kernel (one object file each); every other
@@ -47,7 +46,8 @@ struct EdgeKernelParams {
 
 struct EdgeKernelEntry {
   const void* fn;      // __global__ edge_kernel<N>
-  int block;           // threads per CTA (= edges per tile)
+  int block;           // threads per CTA (consumer warps + one producer warp)
+  int tile;            // edges per tile
   size_t ring_bytes;   // shared memory of the TMA ring
   int rank;            // N of the instantiation (0 = generic)
 };
@@ -58,8 +58,8 @@ EdgeKernelEntry edge_entry_0();
 
 // launchers (kernels.cu)
 EdgeKernelEntry edge_entry(int N);
-// dynamic shared memory of the edge kernel for hot tiers T, H
-size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int T, int H);
+// dynamic shared memory of the edge kernel with H shared accumulators
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int H);
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
                                cudaStream_t s);

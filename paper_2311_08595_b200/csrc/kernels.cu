@@ -103,8 +103,8 @@ EdgeKernelEntry edge_entry(int N) {
   }
 }
 
-size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int T, int H) {
-  return e.ring_bytes + (size_t)(T * e.block + H) * sizeof(double);
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int H) {
+  return e.ring_bytes + (size_t)H * sizeof(double);
 }
 
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm) {

@@ -13,7 +13,10 @@
 #include <nccl.h>
 #include <omp.h>
 
+#include <parallel/algorithm>
+
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -211,7 +214,6 @@ struct sttsv_plan_s {
   double* d_xa = nullptr;
   double* d_ya = nullptr;
   double* d_scratch = nullptr;
-  int32_t* d_counter = nullptr;
   // e2e staging (sttsv_apply_host)
   double* d_xhost = nullptr;
   double* d_yhost = nullptr;
@@ -397,15 +399,23 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   }
   std::vector<int32_t> h_ids((size_t)ids_total, 0);
   std::vector<double> h_w((size_t)w_total, 0.0);
-  std::vector<double> Ck(N + 1, 0.0);
   std::vector<long double> Ckl(N + 1, 0.0L);
   for (int k = 1; k <= N; ++k) Ckl[k] = scale_constant(N, k);
+  // rows: this shard's edges, row-major per bucket, members relabelled and ascending
+  std::vector<int64_t> row_off(N + 1, 0);
+  int64_t rows_total = 0;
+  for (int k = 1; k <= N; ++k) {
+    row_off[k] = rows_total;
+    rows_total += (int64_t)k * mk[k];
+  }
+  std::vector<int32_t> rows((size_t)rows_total);
+  std::vector<double> wrow((size_t)w_total);
 #pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < m; ++e) {
     const int k = sizes[e];
     const int64_t le = pos[e] - lo[k];
     if (le < 0 || le >= mk[k]) continue;
-    int32_t v[STTSV_MAX_RANK];
+    int32_t* v = rows.data() + row_off[k] + le * k;
     for (int i = 0; i < k; ++i) v[i] = newid[idx[off[e] + i]];
     for (int i = 1; i < k; ++i) {  // members ascending by relabelled id
       int32_t t = v[i];
@@ -413,24 +423,48 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       while (j >= 0 && v[j] > t) { v[j + 1] = v[j]; --j; }
       v[j + 1] = t;
     }
-    int32_t* col = h_ids.data() + ids_off[k] + le;
-    for (int i = 0; i < k; ++i) col[(int64_t)i * stride[k]] = v[i];
     const long double w = weights ? (long double)weights[e] : (long double)k;
-    h_w[w_off[k] + le] = (double)(w * Ckl[k]);
+    wrow[w_off[k] + le] = (double)(w * Ckl[k]);
   }
+  // Sort each bucket lexicographically (stable: the plan is deterministic).
+  // Consecutive edges then share their hot low slots, which the kernel's
+  // warp-segmented scatter turns into one deposit per run.
+  for (int k = 1; k <= N; ++k) {
+    if (mk[k] == 0) continue;
+    const int32_t* R = rows.data() + row_off[k];
+    std::vector<int64_t> perm(mk[k]);
+    std::iota(perm.begin(), perm.end(), (int64_t)0);
+    __gnu_parallel::stable_sort(perm.begin(), perm.end(), [R, k](int64_t a, int64_t b) {
+      const int32_t* x = R + a * k;
+      const int32_t* y = R + b * k;
+      for (int i = 0; i < k; ++i)
+        if (x[i] != y[i]) return x[i] < y[i];
+      return false;
+    });
+    int32_t* col = h_ids.data() + ids_off[k];
+    const int64_t st = stride[k];
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < mk[k]; ++j) {
+      const int32_t* src = R + perm[j] * k;
+      for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = src[i];
+      h_w[w_off[k] + j] = wrow[w_off[k] + perm[j]];
+    }
+  }
+  std::vector<int32_t>().swap(rows);
+  std::vector<double>().swap(wrow);
   std::vector<int32_t>().swap(newid);
 
   // ---- tile order: most expensive buckets first (dynamic scheduler, LPT-like)
   int occ = 0;
-  const int T = (int)std::min<int64_t>(16, na);
+  const int T = 8;  // register tier: slot i holding vertex i, i < 8 (edge_kernel.cuh kDiag)
   const int H = (int)std::max<int64_t>(T, std::min<int64_t>(na, 4096));
   p->ent = edge_entry(N);
-  const int block = p->ent.block;
+  const int tile = p->ent.tile;
   {
     DeviceGuard g(device);
     cudaError_t e0 = cudaSetDevice(device);
     if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "cudaSetDevice"); }
-    p->smem = edge_kernel_smem_bytes(p->ent, T, H);
+    p->smem = edge_kernel_smem_bytes(p->ent, H);
     e0 = edge_kernel_config(p->ent, p->smem, &occ);
     if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "edge kernel configuration"); }
     if (occ < 1) { free_plan(p); return fail(STTSV_ERR_CUDA, "edge kernel cannot be resident (smem %zu)", p->smem); }
@@ -453,14 +487,14 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     b.tile_begin = tiles;
     b.ids_off = ids_off[k];
     b.w_off = w_off[k];
-    tiles += (mk[k] + block - 1) / block;
+    tiles += (mk[k] + tile - 1) / tile;
     fma += dp_fma(N, k) * (double)mk[k];
   }
   kp.num_tiles = tiles;
   kp.n_active = (int32_t)na;
   kp.T = T;
   kp.H = H;
-  kp.tile_edges = block;
+  kp.tile_edges = tile;
   p->fma = fma;
   p->stream_bytes = ids_total * 4 + w_total * 8;
 
@@ -468,9 +502,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   DeviceGuard g(device);
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t b_ids = align(ids_total * 4), b_w = align(w_total * 8), b_act = align(na * 4 + 4),
-               b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8),
-               b_cnt = align(16);
-  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_cnt;
+               b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8);
+  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -480,7 +513,6 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->d_xa = (double*)(base + b_ids + b_w + b_act);
   p->d_ya = (double*)(base + b_ids + b_w + b_act + b_xa);
   p->d_scratch = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya);
-  p->d_counter = (int32_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
   if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
@@ -489,14 +521,13 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.w = d_w;
   kp.xa = p->d_xa;
   kp.ya = p->d_ya;
-  kp.tile_counter = p->d_counter;
 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int64_t grid = (int64_t)sms * std::max(occ, 1);
   if (grid > tiles) grid = std::max<int64_t>(tiles, 1);
   p->grid = (int)grid;
-  p->block = block;
+  p->block = p->ent.block;
   *out = p;
   return STTSV_OK;
 }
@@ -571,7 +602,6 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
   if (p->n_active == 0) return STTSV_OK;
   CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
   if (p->kp.num_tiles > 0) {
-    CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int32_t), s), "memset counter");
     std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
     if (p->profiling) {
       if (p->events_used == p->events.size()) {

