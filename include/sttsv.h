@@ -148,7 +148,7 @@ typedef struct {
   int64_t device_bytes;    /* device memory owned by the plan                            */
   int64_t stream_bytes;    /* bytes of the edge stream one apply reads (ids + weights)   */
   double  fma_per_apply;   /* FP64 fused multiply-adds of the per-edge DP per apply      */
-  int32_t hot_private;     /* T: ids below T accumulate in thread-private slots         */
+  int32_t hot_private;     /* slots 0..T-1 of every edge accumulate in per-lane register runs */
   int32_t hot_shared;      /* H: ids below H accumulate in CTA shared memory            */
   int32_t kernel_grid;     /* CTAs of the edge kernel                                    */
   int32_t kernel_block;    /* threads per CTA of the edge kernel                         */

@@ -14,8 +14,9 @@
 // Q_v = P_{i-1} S_{i+1} with prefix products P_i = g_0..g_i and suffix products
 // S_i = g_i..g_{K-1}; [t^D] of a product is a length-L dot product.
 //
-// dp_edge<K, L> returns c_i = Q_{u_i}[D] + F[D-1]  (WITHOUT the (N-1)!/|beta|
-// factor: the planner folds (N-1)!/|beta(K)| into the stored weight w').
+// dp_edge<K, L> returns q_i = Q_{u_i}[D] and F = F[D-1], so c_i = q_i + F
+// (WITHOUT the (N-1)!/|beta| factor: the planner folds (N-1)!/|beta(K)| into
+// the stored weight w'; the kernel forms w' c_i = fma(w', q_i, w' F)).
 // All loops are over compile-time bounds, so the arrays live in registers.
 #pragma once
 
@@ -50,17 +51,19 @@ __device__ __forceinline__ double coef(const double (&a)[L], const double (&b)[L
 }
 
 template <int K, int L>
-__device__ __forceinline__ void dp_edge(const double (&x)[K], double (&c)[K]) {
+__device__ __forceinline__ void dp_edge(const double (&x)[K], double (&q)[K], double& F) {
   constexpr int D = L - 1;
+  F = 0.0;
   if constexpr (K == 1) {
-    // singleton: Q = 1 (empty product), F = g_0:  c = [D==0] + g_0[D-1] = x^{N-1}/(N-1)!
+    // singleton: Q = 1 (empty product), F = g_0:  q = [D == 0],  F[D-1] = x^D / D!
     if constexpr (D == 0) {
-      c[0] = 1.0;
+      q[0] = 1.0;
     } else {
+      q[0] = 0.0;
       double pw = x[0];
 #pragma unroll
       for (int j = 1; j < D; ++j) pw *= x[0];
-      c[0] = pw * inv_fact_c(D);
+      F = pw * inv_fact_c(D);
     }
   } else {
     double g[K][L];
@@ -75,10 +78,9 @@ __device__ __forceinline__ void dp_edge(const double (&x)[K], double (&c)[K]) {
       }
     }
     if constexpr (K == 2) {
-      double F = 0.0;
       if constexpr (D >= 1) F = coef<D - 1, L>(g[0], g[1]);
-      c[0] = g[1][D] + F;
-      c[1] = g[0][D] + F;
+      q[0] = g[1][D];
+      q[1] = g[0][D];
     } else {
       // prefixes P[i] = g_0 * ... * g_i, i = 0..K-3
       double P[K - 2][L];
@@ -87,27 +89,24 @@ __device__ __forceinline__ void dp_edge(const double (&x)[K], double (&c)[K]) {
 #pragma unroll
       for (int i = 1; i <= K - 3; ++i) trunc_mul<L>(P[i - 1], g[i], P[i]);
       // last two members
-      c[K - 1] = coef<D, L>(P[K - 3], g[K - 2]);   // [t^D] P_{K-2}
-      c[K - 2] = coef<D, L>(P[K - 3], g[K - 1]);   // [t^D] P_{K-3} S_{K-1}
+      q[K - 1] = coef<D, L>(P[K - 3], g[K - 2]);   // [t^D] P_{K-2}
+      q[K - 2] = coef<D, L>(P[K - 3], g[K - 1]);   // [t^D] P_{K-3} S_{K-1}
       double S[L];
       trunc_mul<L>(g[K - 2], g[K - 1], S);          // S_{K-2}
-      double F = 0.0;
       if constexpr (D >= 1) F = coef<D - 1, L>(P[K - 3], S);   // [t^{D-1}] P_{K-3} S_{K-2}
 #pragma unroll
       for (int i = K - 3; i >= 1; --i) {
-        c[i] = coef<D, L>(P[i - 1], S);            // [t^D] P_{i-1} S_{i+1}
+        q[i] = coef<D, L>(P[i - 1], S);            // [t^D] P_{i-1} S_{i+1}
         if (i > 1) {
           double T[L];
           trunc_mul<L>(g[i], S, T);                 // S_i
 #pragma unroll
           for (int j = 0; j < L; ++j) S[j] = T[j];
         } else {
-          c[0] = coef<D, L>(g[1], S);               // [t^D] S_1 = [t^D] g_1 S_2
+          q[0] = coef<D, L>(g[1], S);               // [t^D] S_1 = [t^D] g_1 S_2
         }
       }
-      if constexpr (K == 3) c[0] = S[D];           // S = S_1
-#pragma unroll
-      for (int i = 0; i < K; ++i) c[i] += F;
+      if constexpr (K == 3) q[0] = S[D];           // S = S_1
     }
   }
 }

@@ -18,6 +18,7 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.tile = EdgeCfg<STTSV_INST_N>::TILE;
   e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::STAGES * EdgeCfg<STTSV_INST_N>::STAGE_BYTES;
   e.rank = STTSV_INST_N;
+  e.run_slots = STTSV_INST_N > 0 ? EdgeCfg<STTSV_INST_N>::RMAX : 0;
   return e;
 }
 }  // namespace sttsv

@@ -3,26 +3,32 @@
 // Work decomposition.  The plan stores each cardinality bucket k as SoA int32
 // id columns + fp64 weights w' = w (N-1)!/|beta(k)| (PAPER.md:342 footnote and
 // Alg. 2's factor), edges sorted lexicographically by their
-// (degree-relabelled, ascending) member ids.  A tile is TILE = 32*NCW
+// (degree-relabelled, ascending) member ids.  A tile is TILE = 32*NCW*EPL
 // consecutive edges of one bucket; tiles are ordered most-expensive bucket
-// first and dealt to the persistent CTAs round-robin.
+// first and dealt to the persistent CTAs round-robin (CTA b takes tiles
+// b, b+G, b+2G, ... so its bucket index only moves forward).
 //
 // Warp specialisation.  Per CTA, one producer warp streams tiles into an
 // STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk ->
 // SASS UBLKCP, completion on a `full` mbarrier with expect_tx); NCW consumer
-// warps each take 32 edges of the tile (one edge per lane), run the fully
-// unrolled register DP of dp.cuh for (k, L = N-k+1), and release the stage on
-// an `empty` mbarrier.  No CTA-wide barrier sits on the tile loop.
+// warps each take a contiguous block of 32*EPL edges of the tile (one edge per
+// lane per step, EPL steps), run the fully unrolled register DP of dp.cuh for
+// (k, L = N-k+1), and release the stage on an `empty` mbarrier.  No CTA-wide
+// barrier sits on the tile loop; bucket dispatch is once per tile.
 //
-// Scatter.  Because edges are sorted, the 32 lanes of a warp mostly hold the
-// SAME vertex in a given slot (the hottest vertices sit in the low slots).
-// For each slot the warp reduces its 32 contributions over runs of equal
-// adjacent ids (a shuffle butterfly when the whole warp is one run, else a
-// segmented suffix scan), and only each run's head lane deposits:
-//   slot i holds vertex i (i < kDiag)  -> register accumulator racc[i]
-//   id < H                             -> CTA shared accumulator sacc (atomicAdd)
-//   id >= H                            -> red.global.add.f64 into y_a
-// Each CTA flushes racc and sacc into y_a once, after its last tile.
+// Scatter (row a5).  Contribution d_i = w' c_i goes to vertex id[i] of slot i.
+// Because edges are sorted, a lane sees long runs of the same vertex in the low
+// slots.  Each lane keeps, per slot i < RMAX, a register run accumulator
+// (rid[i], run[i]); a contribution to the same vertex is one DADD.  Only when a
+// run ends (or for slots >= RMAX) is a value flushed: the warp (if any lane
+// flushes) reduces the flushed values over lanes holding the same vertex
+// (adjacent lanes hold adjacent sorted edges, so equal ids are contiguous:
+// segmented suffix scan with shuffles), and each segment head deposits once —
+// into the CTA shared accumulator sacc[v] for v < H (hot, degree-relabelled
+// ids), else with red.global.add.f64 into y_a.  Each CTA flushes sacc once.
+// SASS note: shared fp64 atomicAdd is a CAS loop on sm_100a (ATOMS.CAST.SPIN.64),
+// global is native (REDG.E.ADD.F64); the warp pre-reduction keeps same-address
+// collisions in the CAS loop rare.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,18 +39,21 @@
 
 namespace sttsv {
 
-constexpr int kDiag = 8;
 constexpr unsigned kFull = 0xffffffffu;
 
 template <int N>
 struct EdgeCfg {
-  static constexpr int NCW = (N >= 1 && N <= 16) ? 8 : 4;  // consumer warps
-  static constexpr int TILE = 32 * NCW;                    // edges per tile
-  static constexpr int THREADS = TILE + 32;                // + one producer warp
   static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
-  static constexpr int STAGES = 4;
-  static constexpr int MIN_BLOCKS = 2;
+  static constexpr int NCW = (N >= 1 && N <= 10) ? 15 : 7;  // consumer warps (+1 producer: 4 or 2 warps per SMSP)
+  static constexpr int EPL = 2;                             // edges per lane per tile
+  static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
+  static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
   static constexpr int STAGE_BYTES = TILE * (4 * KMAX + 8);
+  static constexpr int RING_BUDGET = 190 * 1024;
+  static constexpr int STAGES_FIT = RING_BUDGET / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
+  static constexpr int RMAX = KMAX < 8 ? KMAX : 8;          // slots with a register run accumulator
+  static constexpr int MIN_BLOCKS = 1;
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -80,28 +89,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ------------------------------------------------------------ scatter
-__device__ __forceinline__ void deposit_run(int slot, int v, double d, double (&racc)[kDiag],
-                                            double* __restrict__ sacc, double* __restrict__ ya, int H) {
-  if (slot < kDiag && v == slot) {
-#pragma unroll
-    for (int q = 0; q < kDiag; ++q)
-      if (q == slot) racc[q] += d;
-  } else if (v < H) {
-    atomicAdd(&sacc[v], d);
-  } else {
-    atomicAdd(&ya[v], d);
-  }
+__device__ __forceinline__ void deposit(int v, double d, double* __restrict__ sacc, double* __restrict__ ya, int H) {
+  if (v < H) atomicAdd(&sacc[v], d);
+  else atomicAdd(&ya[v], d);
 }
 
-// Reduce (v, d) over the warp's runs of equal adjacent v; each run's first
-// lane deposits the run total.  v < 0 marks an empty lane (ragged tail).
-__device__ __forceinline__ void warp_deposit(int slot, int v, double d, int lane, double (&racc)[kDiag],
-                                             double* __restrict__ sacc, double* __restrict__ ya, int H) {
+// Warp-cooperative flush: lanes with v >= 0 hold a value d for vertex v.
+// Reduce over runs of equal adjacent v (v < 0 breaks runs); each run's first
+// lane deposits the run total.  Must be called by the whole warp.
+__device__ __forceinline__ void warp_flush(int v, double d, int lane, double* __restrict__ sacc,
+                                           double* __restrict__ ya, int H) {
   const int v0 = __shfl_sync(kFull, v, 0);
   if (__all_sync(kFull, v == v0)) {
+    if (v0 < 0) return;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
-    if (lane == 0 && v >= 0) deposit_run(slot, v, d, racc, sacc, ya, H);
+    if (lane == 0) deposit(v0, d, sacc, ya, H);
     return;
   }
   // segmented suffix scan: after the loop a lane holds the sum from itself to
@@ -118,44 +121,89 @@ __device__ __forceinline__ void warp_deposit(int slot, int v, double d, int lane
     }
   }
   const int vp = __shfl_up_sync(kFull, v, 1);
-  if ((lane == 0 || vp != v) && v >= 0) deposit_run(slot, v, d, racc, sacc, ya, H);
+  if ((lane == 0 || vp != v) && v >= 0) deposit(v, d, sacc, ya, H);
 }
 
-// 32 edges of a size-K bucket, one per lane, from the shared stage
-template <int N, int K, int TILE>
+template <int RMAX>
+struct RunAcc {
+  int rid[RMAX];
+  double run[RMAX];
+};
+
+// slot I of the current edge: (v, d); v < 0 for an empty lane (d = 0)
+template <int I, int RMAX>
+__device__ __forceinline__ void slot_deposit(int v, double d, RunAcc<RMAX>& ra, int lane, double* sacc, double* ya,
+                                             int H) {
+  int fv;
+  double fd;
+  if constexpr (I < RMAX) {
+    const bool same = (v == ra.rid[I]) | (v < 0);
+    fv = same ? -1 : ra.rid[I];
+    fd = ra.run[I];
+    ra.run[I] = same ? ra.run[I] + d : d;
+    ra.rid[I] = same ? ra.rid[I] : v;
+  } else {
+    fv = v;
+    fd = d;
+  }
+  if (__any_sync(kFull, fv >= 0)) warp_flush(fv, fd, lane, sacc, ya, H);
+}
+
+template <int I, int K, int RMAX>
+__device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (&dv)[K], RunAcc<RMAX>& ra, int lane,
+                                              double* sacc, double* ya, int H) {
+  if constexpr (I < K) {
+    slot_deposit<I, RMAX>(id[I], dv[I], ra, lane, sacc, ya, H);
+    slots_deposit<I + 1, K, RMAX>(id, dv, ra, lane, sacc, ya, H);
+  }
+}
+
+// EPL*32 edges of a size-K bucket: this warp's block of the staged tile,
+// one edge per lane per step.
+template <int N, int K, int TILE, int EPL, int RMAX>
 __device__ __forceinline__ void warp_edges(const int32_t* __restrict__ sids, const double* __restrict__ sw,
-                                           int col, bool valid, const double* __restrict__ xa,
-                                           double (&racc)[kDiag], double* sacc, double* ya, int H, int lane) {
+                                           int col0, int nvalid, const double* __restrict__ xa, RunAcc<RMAX>& ra,
+                                           double* sacc, double* ya, int H, int lane) {
   constexpr int L = N - K + 1;
-  int id[K];
-  double x[K], c[K];
+#pragma unroll 1
+  for (int r = 0; r < EPL; ++r) {
+    const int col = col0 + r * 32 + lane;
+    const bool valid = r * 32 + lane < nvalid;
+    if (!__any_sync(kFull, valid)) break;
+    int id[K];
+    double x[K], q[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) id[i] = valid ? sids[i * TILE + col] : -1;
+    for (int i = 0; i < K; ++i) id[i] = valid ? sids[i * TILE + col] : -1;
 #pragma unroll
-  for (int i = 0; i < K; ++i) x[i] = valid ? __ldg(xa + id[i]) : 0.0;
-  const double w = valid ? sw[col] : 0.0;
-  dp_edge<K, L>(x, c);
+    for (int i = 0; i < K; ++i) x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+    const double w = valid ? sw[col] : 0.0;
+    double F;
+    dp_edge<K, L>(x, q, F);
+    const double wF = w * F;
+    double dv[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) warp_deposit(i, id[i], w * c[i], lane, racc, sacc, ya, H);
+    for (int i = 0; i < K; ++i) dv[i] = fma(w, q[i], wF);
+    slots_deposit<0, K, RMAX>(id, dv, ra, lane, sacc, ya, H);
+  }
 }
 
-template <int N, int K, int TILE>
-__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int col, bool valid,
-                                           const double* xa, double (&racc)[kDiag], double* sacc, double* ya,
-                                           int H, int lane) {
+template <int N, int K, int TILE, int EPL, int RMAX>
+__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int col0, int nvalid,
+                                           const double* xa, RunAcc<RMAX>& ra, double* sacc, double* ya, int H,
+                                           int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      warp_edges<N, K, TILE>(sids, sw, col, valid, xa, racc, sacc, ya, H, lane);
+      warp_edges<N, K, TILE, EPL, RMAX>(sids, sw, col0, nvalid, xa, ra, sacc, ya, H, lane);
       return;
     }
-    dispatch_k<N, K + 1, TILE>(k, sids, sw, col, valid, xa, racc, sacc, ya, H, lane);
+    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, xa, ra, sacc, ya, H, lane);
   }
 }
 
 // ---------------------------------------------------------------- generic
 // Runtime (K, L) DP for ranks without a compiled specialisation: same
-// recurrence as dp_edge, arrays in local memory.
-static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* x, double* c) {
+// recurrence as dp_edge, arrays in local memory.  Returns q_i = Q_i[D] and F = F[D-1].
+static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* x, double* q, double* Fout) {
   const int D = L - 1;
   double g[STTSV_MAX_RANK][STTSV_MAX_RANK];
   for (int i = 0; i < K; ++i) {
@@ -168,14 +216,9 @@ static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* 
     }
   }
   if (K == 1) {
-    if (D == 0) {
-      c[0] = 1.0;
-    } else {
-      double pw = x[0], f = 1.0;
-      for (int j = 1; j < D; ++j) pw *= x[0];
-      for (int j = 2; j <= D; ++j) f *= double(j);
-      c[0] = pw / f;
-    }
+    // q = [t^D] (empty product) = [D == 0];  F = [t^{D-1}] g_0 = x^D / D!
+    q[0] = D == 0 ? 1.0 : 0.0;
+    *Fout = D >= 1 ? g[0][D - 1] : 0.0;
     return;
   }
   auto coefD = [&](const double* a, const double* b, int deg) {
@@ -191,46 +234,51 @@ static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* 
     }
   };
   if (K == 2) {
-    double F = D >= 1 ? coefD(g[0], g[1], D - 1) : 0.0;
-    c[0] = g[1][D] + F;
-    c[1] = g[0][D] + F;
+    *Fout = D >= 1 ? coefD(g[0], g[1], D - 1) : 0.0;
+    q[0] = g[1][D];
+    q[1] = g[0][D];
     return;
   }
   double P[STTSV_MAX_RANK][STTSV_MAX_RANK];
   for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
   for (int i = 1; i <= K - 3; ++i) tmul(P[i - 1], g[i], P[i]);
-  c[K - 1] = coefD(P[K - 3], g[K - 2], D);
-  c[K - 2] = coefD(P[K - 3], g[K - 1], D);
+  q[K - 1] = coefD(P[K - 3], g[K - 2], D);
+  q[K - 2] = coefD(P[K - 3], g[K - 1], D);
   double S[STTSV_MAX_RANK], T[STTSV_MAX_RANK];
   tmul(g[K - 2], g[K - 1], S);
-  double F = D >= 1 ? coefD(P[K - 3], S, D - 1) : 0.0;
+  *Fout = D >= 1 ? coefD(P[K - 3], S, D - 1) : 0.0;
   for (int i = K - 3; i >= 1; --i) {
-    c[i] = coefD(P[i - 1], S, D);
+    q[i] = coefD(P[i - 1], S, D);
     if (i > 1) {
       tmul(g[i], S, T);
       for (int j = 0; j < L; ++j) S[j] = T[j];
     } else {
-      c[0] = coefD(g[1], S, D);
+      q[0] = coefD(g[1], S, D);
     }
   }
-  if (K == 3) c[0] = S[D];
-  for (int i = 0; i < K; ++i) c[i] += F;
+  if (K == 3) q[0] = S[D];
 }
 
-
-template <int TILE>
-__device__ __forceinline__ void warp_edges_generic(int N, int k, const int32_t* sids, const double* sw, int col,
-                                                   bool valid, const double* xa, double (&racc)[kDiag],
-                                                   double* sacc, double* ya, int H, int lane) {
-  int id[STTSV_MAX_RANK];
-  double x[STTSV_MAX_RANK], c[STTSV_MAX_RANK];
-  for (int i = 0; i < k; ++i) {
-    id[i] = valid ? sids[i * TILE + col] : -1;
-    x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+template <int TILE, int EPL>
+__device__ __forceinline__ void warp_edges_generic(int N, int k, const int32_t* sids, const double* sw, int col0,
+                                                   int nvalid, const double* xa, double* sacc, double* ya, int H,
+                                                   int lane) {
+  for (int r = 0; r < EPL; ++r) {
+    const int col = col0 + r * 32 + lane;
+    const bool valid = r * 32 + lane < nvalid;
+    if (!__any_sync(kFull, valid)) break;
+    int id[STTSV_MAX_RANK];
+    double x[STTSV_MAX_RANK], q[STTSV_MAX_RANK];
+    for (int i = 0; i < k; ++i) {
+      id[i] = valid ? sids[i * TILE + col] : -1;
+      x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+    }
+    double F = 0.0;
+    dp_edge_generic(k, N - k + 1, x, q, &F);
+    const double w = valid ? sw[col] : 0.0;
+    const double wF = w * F;
+    for (int i = 0; i < k; ++i) warp_flush(id[i], fma(w, q[i], wF), lane, sacc, ya, H);
   }
-  dp_edge_generic(k, N - k + 1, x, c);
-  const double w = valid ? sw[col] : 0.0;
-  for (int i = 0; i < k; ++i) warp_deposit(i, id[i], w * c[i], lane, racc, sacc, ya, H);
 }
 
 // ------------------------------------------------------------- the kernel
@@ -239,7 +287,8 @@ template <int N>
 __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     edge_kernel(const __grid_constant__ EdgeKernelParams p) {
   using Cfg = EdgeCfg<N>;
-  constexpr int TILE = Cfg::TILE, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX, NCW = Cfg::NCW;
+  constexpr int TILE = Cfg::TILE, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX, NCW = Cfg::NCW, EPL = Cfg::EPL;
+  constexpr int RMAX = Cfg::RMAX;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ] | sacc [H] f64
   unsigned char* ring = smem_raw;
@@ -262,10 +311,10 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     // ---------------- producer warp: TMA bulk copies of tile t into stage it % STAGES
     if (lane == 0) {
       int64_t it = 0;
+      int b = 0;
       for (int64_t t = blockIdx.x; t < p.num_tiles; t += G, ++it) {
         const int s = (int)(it % STAGES);
         if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
-        int b = 0;
         while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const BucketDesc& bd = p.b[b];
         const int64_t e0 = (t - bd.tile_begin) * TILE;
@@ -281,40 +330,39 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     }
   } else {
     // ---------------- consumer warps
-    double racc[kDiag];
+    RunAcc<RMAX> ra;
 #pragma unroll
-    for (int i = 0; i < kDiag; ++i) racc[i] = 0.0;
+    for (int i = 0; i < RMAX; ++i) {
+      ra.rid[i] = -1;
+      ra.run[i] = 0.0;
+    }
     int64_t it = 0;
+    int b = 0;
     for (int64_t t = blockIdx.x; t < p.num_tiles; t += G, ++it) {
       const int s = (int)(it % STAGES);
-      int b = 0;
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
-      const BucketDesc& bd = p.b[b];
-      const int64_t e0 = (t - bd.tile_begin) * TILE + warp * 32;
+      const int64_t m = p.b[b].m;
+      const int k = p.b[b].k;
+      const int64_t e0 = (t - p.b[b].tile_begin) * TILE + warp * 32 * EPL;
       mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
-      if (e0 < bd.m) {
+      if (e0 < m) {
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
         const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
-        const bool valid = e0 + lane < bd.m;
-        const int col = warp * 32 + lane;
+        const int nvalid = m - e0 < 32 * EPL ? (int)(m - e0) : 32 * EPL;
+        const int col0 = warp * 32 * EPL;
         if constexpr (N > 0) {
-          dispatch_k<N, 1, TILE>(bd.k, sids, sw, col, valid, p.xa, racc, sacc, p.ya, p.H, lane);
+          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, p.xa, ra, sacc, p.ya, p.H, lane);
         } else {
-          warp_edges_generic<TILE>(p.N, bd.k, sids, sw, col, valid, p.xa, racc, sacc, p.ya, p.H, lane);
+          warp_edges_generic<TILE, EPL>(p.N, k, sids, sw, col0, nvalid, p.xa, sacc, p.ya, p.H, lane);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // fold the register accumulators (vertex i < kDiag exists whenever racc[i] != 0, and H >= min(n_a, kDiag))
+    // flush the run accumulators
 #pragma unroll
-    for (int i = 0; i < kDiag; ++i) {
-      double v = racc[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-      if (lane == 0 && v != 0.0) atomicAdd(&sacc[i], v);
-    }
+    for (int i = 0; i < RMAX; ++i) warp_flush(ra.rid[i], ra.run[i], lane, sacc, p.ya, p.H);
   }
   __syncthreads();
   for (int j = tid; j < p.H; j += Cfg::THREADS)

@@ -33,7 +33,7 @@ struct EdgeKernelParams {
   const double* xa;      // x on active vertices (relabelled)
   double* ya;            // y on active vertices (accumulated)
   int32_t n_active;
-  int32_t T;             // register-accumulated slots (slot i holding vertex i, i < T)
+  int32_t T;             // slots with a per-lane register run accumulator (informational)
   int32_t H;             // ids < H: CTA shared-memory accumulators
   int32_t tile_edges;    // edges per tile
   int64_t num_tiles;     // tiles are dealt round-robin to the persistent CTAs
@@ -50,6 +50,7 @@ struct EdgeKernelEntry {
   int tile;            // edges per tile
   size_t ring_bytes;   // shared memory of the TMA ring
   int rank;            // N of the instantiation (0 = generic)
+  int run_slots;       // slots with a register run accumulator (EdgeCfg::RMAX; 0 = none)
 };
 #define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry_##n();
 STTSV_COMPILED_RANKS(STTSV_DECLARE_ENTRY)

@@ -456,9 +456,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
 
   // ---- tile order: most expensive buckets first (dynamic scheduler, LPT-like)
   int occ = 0;
-  const int T = 8;  // register tier: slot i holding vertex i, i < 8 (edge_kernel.cuh kDiag)
-  const int H = (int)std::max<int64_t>(T, std::min<int64_t>(na, 4096));
+  const int H = (int)std::min<int64_t>(na, 4096);
   p->ent = edge_entry(N);
+  const int T = p->ent.run_slots;
   const int tile = p->ent.tile;
   {
     DeviceGuard g(device);
