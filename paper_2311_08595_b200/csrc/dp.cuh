@@ -14,10 +14,13 @@
 // Q_v = P_{i-1} S_{i+1} with prefix products P_i = g_0..g_i and suffix products
 // S_i = g_i..g_{K-1}; [t^D] of a product is a length-L dot product.
 //
-// dp_edge<K, L> returns q_i = Q_{u_i}[D] and F = F[D-1], so c_i = q_i + F
-// (WITHOUT the (N-1)!/|beta| factor: the planner folds (N-1)!/|beta(K)| into
-// the stored weight w'; the kernel forms w' c_i = fma(w', q_i, w' F)).
-// All loops are over compile-time bounds, so the arrays live in registers.
+// The series g of every active vertex is tabulated once per apply (gather /
+// normalize kernels, `series_row`), so the edge kernel loads g rows instead of
+// recomputing powers per incidence.  dp_core<K, L> returns q_i = Q_{u_i}[D] and
+// F = F[D-1], so c_i = q_i + F (WITHOUT the (N-1)!/|beta| factor: the planner
+// folds (N-1)!/|beta(K)| into the stored weight w'; the kernel forms
+// w' c_i = fma(w', q_i, w' F)).  All loops are over compile-time bounds, so the
+// arrays live in registers.
 #pragma once
 
 namespace sttsv {
@@ -26,6 +29,30 @@ __device__ __forceinline__ constexpr double inv_fact_c(int j) {
   double f = 1.0;
   for (int i = 2; i <= j; ++i) f *= double(i);
   return 1.0 / f;
+}
+
+// g[j] = x^{j+1}/(j+1)!, j = 0..GS-1 (the table writer)
+__device__ __forceinline__ void series_row(double x, double* __restrict__ g, int GS) {
+  double pw = x, f = 1.0;
+  g[0] = pw;
+  for (int j = 1; j < GS; ++j) {
+    pw *= x;
+    f *= double(j + 1);
+    g[j] = pw * (1.0 / f);
+  }
+}
+
+// load coefficients 0..L-1 of one table row with 16-byte loads (rows are 16-B
+// aligned with an even stride >= L, so an odd L reads one padding coefficient)
+template <int L>
+__device__ __forceinline__ void load_series(const double* __restrict__ row, double (&g)[L]) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+  for (int j = 0; j < L; j += 2) {
+    const double2 v = __ldg(r2 + j / 2);
+    g[j] = v.x;
+    if (j + 1 < L) g[j + 1] = v.y;
+  }
 }
 
 // truncated product r = (a*b) mod t^L
@@ -50,64 +77,58 @@ __device__ __forceinline__ double coef(const double (&a)[L], const double (&b)[L
   return s;
 }
 
+// K >= 2 members with series g[i][0..L-1]
 template <int K, int L>
-__device__ __forceinline__ void dp_edge(const double (&x)[K], double (&q)[K], double& F) {
+__device__ __forceinline__ void dp_core(const double (&g)[K][L], double (&q)[K], double& F) {
+  static_assert(K >= 2, "dp_core needs K >= 2");
   constexpr int D = L - 1;
   F = 0.0;
+  if constexpr (K == 2) {
+    if constexpr (D >= 1) F = coef<D - 1, L>(g[0], g[1]);
+    q[0] = g[1][D];
+    q[1] = g[0][D];
+  } else {
+    // prefixes P[i] = g_0 * ... * g_i, i = 0..K-3
+    double P[K - 2][L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
+#pragma unroll
+    for (int i = 1; i <= K - 3; ++i) trunc_mul<L>(P[i - 1], g[i], P[i]);
+    // last two members
+    q[K - 1] = coef<D, L>(P[K - 3], g[K - 2]);   // [t^D] P_{K-2}
+    q[K - 2] = coef<D, L>(P[K - 3], g[K - 1]);   // [t^D] P_{K-3} S_{K-1}
+    double S[L];
+    trunc_mul<L>(g[K - 2], g[K - 1], S);          // S_{K-2}
+    if constexpr (D >= 1) F = coef<D - 1, L>(P[K - 3], S);   // [t^{D-1}] P_{K-3} S_{K-2}
+#pragma unroll
+    for (int i = K - 3; i >= 1; --i) {
+      q[i] = coef<D, L>(P[i - 1], S);            // [t^D] P_{i-1} S_{i+1}
+      if (i > 1) {
+        double T[L];
+        trunc_mul<L>(g[i], S, T);                 // S_i
+#pragma unroll
+        for (int j = 0; j < L; ++j) S[j] = T[j];
+      } else {
+        q[0] = coef<D, L>(g[1], S);               // [t^D] S_1 = [t^D] g_1 S_2
+      }
+    }
+    if constexpr (K == 3) q[0] = S[D];           // S = S_1
+  }
+}
+
+// One edge from the series table: rows[i] = table row of member i.
+template <int K, int L>
+__device__ __forceinline__ void dp_edge_table(const double* const (&rows)[K], double (&q)[K], double& F) {
+  constexpr int D = L - 1;
   if constexpr (K == 1) {
     // singleton: Q = 1 (empty product), F = g_0:  q = [D == 0],  F[D-1] = x^D / D!
-    if constexpr (D == 0) {
-      q[0] = 1.0;
-    } else {
-      q[0] = 0.0;
-      double pw = x[0];
-#pragma unroll
-      for (int j = 1; j < D; ++j) pw *= x[0];
-      F = pw * inv_fact_c(D);
-    }
+    q[0] = D == 0 ? 1.0 : 0.0;
+    F = D >= 1 ? __ldg(rows[0] + (D - 1)) : 0.0;
   } else {
     double g[K][L];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double pw = x[i];
-      g[i][0] = pw;
-#pragma unroll
-      for (int j = 1; j < L; ++j) {
-        pw *= x[i];
-        g[i][j] = pw * inv_fact_c(j + 1);
-      }
-    }
-    if constexpr (K == 2) {
-      if constexpr (D >= 1) F = coef<D - 1, L>(g[0], g[1]);
-      q[0] = g[1][D];
-      q[1] = g[0][D];
-    } else {
-      // prefixes P[i] = g_0 * ... * g_i, i = 0..K-3
-      double P[K - 2][L];
-#pragma unroll
-      for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
-#pragma unroll
-      for (int i = 1; i <= K - 3; ++i) trunc_mul<L>(P[i - 1], g[i], P[i]);
-      // last two members
-      q[K - 1] = coef<D, L>(P[K - 3], g[K - 2]);   // [t^D] P_{K-2}
-      q[K - 2] = coef<D, L>(P[K - 3], g[K - 1]);   // [t^D] P_{K-3} S_{K-1}
-      double S[L];
-      trunc_mul<L>(g[K - 2], g[K - 1], S);          // S_{K-2}
-      if constexpr (D >= 1) F = coef<D - 1, L>(P[K - 3], S);   // [t^{D-1}] P_{K-3} S_{K-2}
-#pragma unroll
-      for (int i = K - 3; i >= 1; --i) {
-        q[i] = coef<D, L>(P[i - 1], S);            // [t^D] P_{i-1} S_{i+1}
-        if (i > 1) {
-          double T[L];
-          trunc_mul<L>(g[i], S, T);                 // S_i
-#pragma unroll
-          for (int j = 0; j < L; ++j) S[j] = T[j];
-        } else {
-          q[0] = coef<D, L>(g[1], S);               // [t^D] S_1 = [t^D] g_1 S_2
-        }
-      }
-      if constexpr (K == 3) q[0] = S[D];           // S = S_1
-    }
+    for (int i = 0; i < K; ++i) load_series<L>(rows[i], g[i]);
+    dp_core<K, L>(g, q, F);
   }
 }
 

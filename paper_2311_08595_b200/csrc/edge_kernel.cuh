@@ -130,73 +130,81 @@ struct RunAcc {
   double run[RMAX];
 };
 
-// slot I of the current edge: (v, d); v < 0 for an empty lane (d = 0)
-template <int I, int RMAX>
-__device__ __forceinline__ void slot_deposit(int v, double d, RunAcc<RMAX>& ra, int lane, double* sacc, double* ya,
-                                             int H) {
-  int fv;
-  double fd;
-  if constexpr (I < RMAX) {
-    const bool same = (v == ra.rid[I]) | (v < 0);
-    fv = same ? -1 : ra.rid[I];
-    fd = ra.run[I];
-    ra.run[I] = same ? ra.run[I] + d : d;
-    ra.rid[I] = same ? ra.rid[I] : v;
-  } else {
-    fv = v;
-    fd = d;
+// Slots of the current edge: (id[i], dv[i]); `valid` false for an empty lane
+// (dv = 0).  Slot i < RMAX feeds its run accumulator and yields a flush
+// (old id, old run) when the id changes; slots >= RMAX flush every value.
+// One REDUX gives the warp-uniform set of slots with any flush.
+template <int K, int RMAX>
+__device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (&dv)[K], bool valid,
+                                              RunAcc<RMAX>& ra, int lane, double* sacc, double* ya, int H) {
+  int fv[K];
+  double fd[K];
+  unsigned lm = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (i < RMAX) {
+      constexpr int R1 = RMAX - 1;
+      const int j = i < RMAX ? i : R1;  // compile-time after unrolling
+      const bool same = (id[i] == ra.rid[j]) | !valid;
+      fv[i] = same ? -1 : ra.rid[j];
+      fd[i] = ra.run[j];
+      ra.run[j] = same ? ra.run[j] + dv[i] : dv[i];
+      ra.rid[j] = same ? ra.rid[j] : id[i];
+    } else {
+      fv[i] = valid ? id[i] : -1;
+      fd[i] = dv[i];
+    }
+    lm |= (fv[i] >= 0 ? 1u : 0u) << i;
   }
-  if (__any_sync(kFull, fv >= 0)) warp_flush(fv, fd, lane, sacc, ya, H);
-}
-
-template <int I, int K, int RMAX>
-__device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (&dv)[K], RunAcc<RMAX>& ra, int lane,
-                                              double* sacc, double* ya, int H) {
-  if constexpr (I < K) {
-    slot_deposit<I, RMAX>(id[I], dv[I], ra, lane, sacc, ya, H);
-    slots_deposit<I + 1, K, RMAX>(id, dv, ra, lane, sacc, ya, H);
+  const unsigned um = __reduce_or_sync(kFull, lm);
+  if (um) {
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (um & (1u << i)) warp_flush(fv[i], fd[i], lane, sacc, ya, H);
   }
 }
 
 // EPL*32 edges of a size-K bucket: this warp's block of the staged tile,
-// one edge per lane per step.
+// one edge per lane per step.  Empty lanes read member ids of column col0
+// (valid table rows) and carry w = 0.
 template <int N, int K, int TILE, int EPL, int RMAX>
 __device__ __forceinline__ void warp_edges(const int32_t* __restrict__ sids, const double* __restrict__ sw,
-                                           int col0, int nvalid, const double* __restrict__ xa, RunAcc<RMAX>& ra,
-                                           double* sacc, double* ya, int H, int lane) {
+                                           int col0, int nvalid, const double* __restrict__ xg, int gs,
+                                           RunAcc<RMAX>& ra, double* sacc, double* ya, int H, int lane) {
   constexpr int L = N - K + 1;
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
-    const int col = col0 + r * 32 + lane;
+    if (r * 32 >= nvalid) break;
     const bool valid = r * 32 + lane < nvalid;
-    if (!__any_sync(kFull, valid)) break;
+    const int col = valid ? col0 + r * 32 + lane : col0;
     int id[K];
-    double x[K], q[K];
+    const double* rows[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) id[i] = valid ? sids[i * TILE + col] : -1;
-#pragma unroll
-    for (int i = 0; i < K; ++i) x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+    for (int i = 0; i < K; ++i) {
+      id[i] = sids[i * TILE + col];
+      rows[i] = xg + (size_t)id[i] * gs;
+    }
     const double w = valid ? sw[col] : 0.0;
-    double F;
-    dp_edge<K, L>(x, q, F);
+    double q[K], F;
+    dp_edge_table<K, L>(rows, q, F);
     const double wF = w * F;
     double dv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) dv[i] = fma(w, q[i], wF);
-    slots_deposit<0, K, RMAX>(id, dv, ra, lane, sacc, ya, H);
+    slots_deposit<K, RMAX>(id, dv, valid, ra, lane, sacc, ya, H);
   }
 }
 
 template <int N, int K, int TILE, int EPL, int RMAX>
 __device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int col0, int nvalid,
-                                           const double* xa, RunAcc<RMAX>& ra, double* sacc, double* ya, int H,
-                                           int lane) {
+                                           const double* xg, int gs, RunAcc<RMAX>& ra, double* sacc, double* ya,
+                                           int H, int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      warp_edges<N, K, TILE, EPL, RMAX>(sids, sw, col0, nvalid, xa, ra, sacc, ya, H, lane);
+      warp_edges<N, K, TILE, EPL, RMAX>(sids, sw, col0, nvalid, xg, gs, ra, sacc, ya, H, lane);
       return;
     }
-    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, xa, ra, sacc, ya, H, lane);
+    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, xg, gs, ra, sacc, ya, H, lane);
   }
 }
 
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         const int nvalid = m - e0 < 32 * EPL ? (int)(m - e0) : 32 * EPL;
         const int col0 = warp * 32 * EPL;
         if constexpr (N > 0) {
-          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, p.xa, ra, sacc, p.ya, p.H, lane);
+          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, p.xg, p.gs, ra, sacc, p.ya, p.H, lane);
         } else {
           warp_edges_generic<TILE, EPL>(p.N, k, sids, sw, col0, nvalid, p.xa, sacc, p.ya, p.H, lane);
         }

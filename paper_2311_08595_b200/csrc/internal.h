@@ -24,6 +24,11 @@ struct BucketDesc {
 
 constexpr int kMaxBuckets = STTSV_MAX_RANK;
 
+// Row stride (doubles) of the per-apply series table x_g (dp.cuh): coefficients
+// j = 0..N-2 are used (L - 1 <= N - 2 for k >= 2; the singleton needs j = N - 2),
+// padded to an even count so rows are 16-byte aligned.
+__host__ __device__ constexpr int series_stride(int N) { return N < 2 ? 2 : ((N - 1 + 1) & ~1); }
+
 struct EdgeKernelParams {
   int32_t N;             // rank
   int32_t nb;            // number of non-empty buckets, in tile order
@@ -31,6 +36,8 @@ struct EdgeKernelParams {
   const int32_t* ids;    // ids pool
   const double* w;       // weight pool
   const double* xa;      // x on active vertices (relabelled)
+  const double* xg;      // series table: row i = g[j] = x_a[i]^{j+1}/(j+1)!, j < gs (dp.cuh)
+  int32_t gs;            // row stride of xg (doubles, even)
   double* ya;            // y on active vertices (accumulated)
   int32_t n_active;
   int32_t T;             // slots with a per-lane register run accumulator (informational)
@@ -64,11 +71,12 @@ size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int H);
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
                                cudaStream_t s);
-cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, int64_t n_active, cudaStream_t s);
+cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
+                          cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // doubles of scratch launch_normalize needs
-cudaError_t launch_normalize(const double* z, double* x, double* partial, int64_t n_active, int N,
-                             cudaStream_t s);
+cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,
+                             int N, cudaStream_t s);
 cudaError_t launch_fill_const(double* y, int64_t n, double v, cudaStream_t s);
 
 }  // namespace sttsv

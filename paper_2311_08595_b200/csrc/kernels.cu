@@ -2,24 +2,29 @@
 // registry (the hot rows a3-a5 live in
 // edge_kernel.cuh, instantiated per rank by edge_inst.cu).
 //
-//   a2 gather      x_a[i] = x[act[i]]                        gather_kernel
+//   a2 gather      x_a[i] = x[act[i]], series table row i        gather_kernel
 //   a7 expand      y[act[i]] = y_a[i]                        expand_kernel
 //   a8 power step  x_a = z_a^[1/(N-1)] / ||.||_1              normalize_{partial,apply}_kernel
 //      (Alg. 1 line 6)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dp.cuh"
 #include "edge_kernel.cuh"
 #include "internal.h"
 
 namespace sttsv {
 
 // ------------------------------------------------------- small kernels
+// x_a[i] = x[act[i]] and the series row g_i[j] = x_a[i]^{j+1}/(j+1)! (dp.cuh)
 __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __restrict__ act,
-                              double* __restrict__ xa, int64_t n_active) {
+                              double* __restrict__ xa, double* __restrict__ xg, int gs, int64_t n_active) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
-       i += (int64_t)gridDim.x * blockDim.x)
-    xa[i] = x[act[i]];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[act[i]];
+    xa[i] = v;
+    series_row(v, xg + i * gs, gs);
+  }
 }
 
 __global__ void expand_kernel(const double* __restrict__ ya, const int32_t* __restrict__ act,
@@ -74,6 +79,7 @@ __global__ void __launch_bounds__(kNormBlock) normalize_partial_kernel(const dou
 
 // every block sums all partials in the same order, then scales its slice
 __global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __restrict__ x,
+                                                                    double* __restrict__ xg, int gs,
                                                                     const double* __restrict__ partial,
                                                                     int nparts, int64_t n) {
   __shared__ double tot;
@@ -86,8 +92,11 @@ __global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __r
   }
   __syncthreads();
   const double t = tot;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = x[i] / t;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i] / t;
+    x[i] = v;
+    series_row(v, xg + i * gs, gs);
+  }
 }
 
 // ------------------------------------------------------------- launchers
@@ -126,9 +135,10 @@ static int grid_for(int64_t n, int block, int cap) {
   return (int)g;
 }
 
-cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, int64_t n_active, cudaStream_t s) {
+cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
+                          cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
-  gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, n_active);
+  gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, n_active);
   return cudaGetLastError();
 }
 
@@ -145,12 +155,12 @@ cudaError_t launch_fill_const(double* y, int64_t n, double v, cudaStream_t s) {
 }
 
 // x and z are n_active long; `partial` holds kNormalizeScratch doubles.
-cudaError_t launch_normalize(const double* z, double* x, double* partial, int64_t n_active, int N,
-                             cudaStream_t s) {
+cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,
+                             int N, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
   const int grid = grid_for(n_active, kNormBlock, kNormMaxGrid);
   normalize_partial_kernel<<<grid, kNormBlock, 0, s>>>(z, x, partial, n_active, 1.0 / double(N - 1));
-  normalize_apply_kernel<<<grid, kNormBlock, 0, s>>>(x, partial, grid, n_active);
+  normalize_apply_kernel<<<grid, kNormBlock, 0, s>>>(x, xg, gs, partial, grid, n_active);
   return cudaGetLastError();
 }
 

@@ -214,6 +214,8 @@ struct sttsv_plan_s {
   double* d_xa = nullptr;
   double* d_ya = nullptr;
   double* d_scratch = nullptr;
+  double* d_xg = nullptr;   // series table (n_active x gs)
+  int gs = 2;
   // e2e staging (sttsv_apply_host)
   double* d_xhost = nullptr;
   double* d_yhost = nullptr;
@@ -503,7 +505,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t b_ids = align(ids_total * 4), b_w = align(w_total * 8), b_act = align(na * 4 + 4),
                b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8);
-  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr;
+  const int gs = series_stride(N);
+  const size_t b_xg = align((size_t)na * gs * 8 + 16);
+  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -513,6 +517,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->d_xa = (double*)(base + b_ids + b_w + b_act);
   p->d_ya = (double*)(base + b_ids + b_w + b_act + b_xa);
   p->d_scratch = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya);
+  p->d_xg = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
+  p->gs = gs;
   if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
@@ -520,6 +526,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.ids = d_ids;
   kp.w = d_w;
   kp.xa = p->d_xa;
+  kp.xg = p->d_xg;
+  kp.gs = gs;
   kp.ya = p->d_ya;
 
   int sms = 148;
@@ -638,7 +646,7 @@ extern "C" sttsv_status_t sttsv_apply(sttsv_plan_t p, const double* x, double* y
   sttsv_status_t st = check_async(p);
   if (st != STTSV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->n_active, s), "gather launch");
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->n_active, s), "gather launch");
   st = apply_active(p, s);
   if (st != STTSV_OK) return st;
   CUDA_TRY(cudaMemsetAsync(y, 0, bytes, s), "memset y");
@@ -676,11 +684,11 @@ extern "C" sttsv_status_t sttsv_power_iterate(sttsv_plan_t p, double* x, double*
   sttsv_status_t st = check_async(p);
   if (st != STTSV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->n_active, s), "gather launch");
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->n_active, s), "gather launch");
   for (int it = 0; it < iters; ++it) {
     st = apply_active(p, s);
     if (st != STTSV_OK) return st;
-    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_scratch, p->n_active, p->N, s), "normalize launch");
+    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_xg, p->gs, p->d_scratch, p->n_active, p->N, s), "normalize launch");
   }
   CUDA_TRY(cudaMemsetAsync(x, 0, bytes, s), "memset x");
   CUDA_TRY(launch_expand(p->d_xa, p->d_act, x, p->n_active, s), "expand x");
