@@ -4,31 +4,32 @@
 // id columns + fp64 weights w' = w (N-1)!/|beta(k)| (PAPER.md:342 footnote and
 // Alg. 2's factor), edges sorted lexicographically by their
 // (degree-relabelled, ascending) member ids.  A tile is TILE = 32*NCW*EPL
-// consecutive edges of one bucket; tiles are ordered most-expensive bucket
-// first and dealt to the persistent CTAs round-robin (CTA b takes tiles
-// b, b+G, b+2G, ... so its bucket index only moves forward).
+// consecutive edges of one bucket.  One persistent CTA per SM takes a
+// CONTIGUOUS, cost-balanced range of tiles [cta_tiles[b], cta_tiles[b+1])
+// (plan.cpp), so consecutive tiles of a CTA are neighbours in the sort order.
 //
 // Warp specialisation.  Per CTA, one producer warp streams tiles into an
 // STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk ->
 // SASS UBLKCP, completion on a `full` mbarrier with expect_tx); NCW consumer
-// warps each take a contiguous block of 32*EPL edges of the tile (one edge per
-// lane per step, EPL steps), run the fully unrolled register DP of dp.cuh for
-// (k, L = N-k+1), and release the stage on an `empty` mbarrier.  No CTA-wide
-// barrier sits on the tile loop; bucket dispatch is once per tile.
+// warps each take a block of 32*EPL edges of the tile, lane l the EPL
+// CONSECUTIVE edges l*EPL .. l*EPL+EPL-1 (EPL odd: the strided shared-memory
+// reads are bank-conflict free), run the fully unrolled register DP of dp.cuh
+// for (k, L = N-k+1), and release the stage on an `empty` mbarrier.  No
+// CTA-wide barrier sits on the tile loop; bucket dispatch is once per tile.
 //
 // Scatter (row a5).  Contribution d_i = w' c_i goes to vertex id[i] of slot i.
-// Because edges are sorted, a lane sees long runs of the same vertex in the low
-// slots.  Each lane keeps, per slot i < RMAX, a register run accumulator
-// (rid[i], run[i]); a contribution to the same vertex is one DADD.  Only when a
-// run ends (or for slots >= RMAX) is a value flushed: the warp (if any lane
-// flushes) reduces the flushed values over lanes holding the same vertex
-// (adjacent lanes hold adjacent sorted edges, so equal ids are contiguous:
-// segmented suffix scan with shuffles), and each segment head deposits once —
-// into the CTA shared accumulator sacc[v] for v < H (hot, degree-relabelled
-// ids), else with red.global.add.f64 into y_a.  Each CTA flushes sacc once.
-// SASS note: shared fp64 atomicAdd is a CAS loop on sm_100a (ATOMS.CAST.SPIN.64),
-// global is native (REDG.E.ADD.F64); the warp pre-reduction keeps same-address
-// collisions in the CAS loop rare.
+// Because edges are sorted and a lane walks consecutive edges, it sees long
+// runs of the same vertex in each slot.  Per slot i < RMAX a lane keeps a
+// register run accumulator (rid[i], run[i]): the same vertex again is one DADD;
+// a different vertex flushes the run.  Flushes inside a tile are per lane (few
+// lanes, distinct vertices); at a tile's first step many lanes can end a run
+// of the same long-run vertex at once.  A flush is ONE predicated, fire-and-
+// forget red.global.add.f64 (SASS REDG.E.ADD.F64; the warp does not wait):
+// for v < H (hot, degree-relabelled ids) into this CTA's private slice
+// priv[cta][v] (L2-resident, contention only inside the CTA), else straight
+// into y_a.  Each CTA adds its slice into y_a once at the end.  (Shared-memory
+// fp64 atomicAdd is a CAS loop on sm_100a — ATOMS.CAST.SPIN.64 — whose latency
+// stalled the warps; there is no native shared fp64 red.)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -44,16 +45,23 @@ constexpr unsigned kFull = 0xffffffffu;
 template <int N>
 struct EdgeCfg {
   static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
-  static constexpr int NCW = (N >= 1 && N <= 10) ? 15 : 7;  // consumer warps (+1 producer: 4 or 2 warps per SMSP)
-  static constexpr int EPL = 2;                             // edges per lane per tile
+  static constexpr int EPL = 5;                             // consecutive edges per lane per tile (odd)
+  static constexpr int EDGE_BYTES = 4 * KMAX + 8;           // staged bytes per edge (ids + w')
+  static constexpr int RING_BUDGET = 220 * 1024;            // dynamic shared memory (<= 227 KB)
+  // consumer warps: 15 (+1 producer = 4 warps per SMSP) for small ranks; fewer
+  // when two stages of the largest bucket would not fit the ring budget
+  static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
+  static constexpr int NCW_PREF = (N >= 1 && N <= 10) ? 15 : 7;
+  static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
-  static constexpr int STAGE_BYTES = TILE * (4 * KMAX + 8);
-  static constexpr int RING_BUDGET = 190 * 1024;
+  static constexpr int STAGE_BYTES = TILE * EDGE_BYTES;
   static constexpr int STAGES_FIT = RING_BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
   static constexpr int RMAX = KMAX < 8 ? KMAX : 8;          // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = 1;
+  static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
+  static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -89,39 +97,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ------------------------------------------------------------ scatter
-__device__ __forceinline__ void deposit(int v, double d, double* __restrict__ sacc, double* __restrict__ ya, int H) {
-  if (v < H) atomicAdd(&sacc[v], d);
-  else atomicAdd(&ya[v], d);
-}
+struct Sink {
+  double* priv;  // this CTA's private slice for ids < H
+  double* ya;    // y on active vertices
+  int H;
+  __device__ __forceinline__ double* at(int v) const { return v < H ? priv + v : ya + v; }
+};
 
-// Warp-cooperative flush: lanes with v >= 0 hold a value d for vertex v.
-// Reduce over runs of equal adjacent v (v < 0 breaks runs); each run's first
-// lane deposits the run total.  Must be called by the whole warp.
-__device__ __forceinline__ void warp_flush(int v, double d, int lane, double* __restrict__ sacc,
-                                           double* __restrict__ ya, int H) {
-  const int v0 = __shfl_sync(kFull, v, 0);
-  if (__all_sync(kFull, v == v0)) {
-    if (v0 < 0) return;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
-    if (lane == 0) deposit(v0, d, sacc, ya, H);
-    return;
-  }
-  // segmented suffix scan: after the loop a lane holds the sum from itself to
-  // the end of its run (f = "my run ends inside the span summed so far")
-  const int vn = __shfl_down_sync(kFull, v, 1);
-  int f = (lane == 31) || (vn != v);
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double dn = __shfl_down_sync(kFull, d, o);
-    const int fn = __shfl_down_sync(kFull, f, o);
-    if (!f && lane + o < 32) {
-      d += dn;
-      f = fn;
-    }
-  }
-  const int vp = __shfl_up_sync(kFull, v, 1);
-  if ((lane == 0 || vp != v) && v >= 0) deposit(v, d, sacc, ya, H);
+__device__ __forceinline__ void red_add(double* a, double d) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(d) : "memory");
 }
 
 template <int RMAX>
@@ -130,53 +114,43 @@ struct RunAcc {
   double run[RMAX];
 };
 
-// Slots of the current edge: (id[i], dv[i]); `valid` false for an empty lane
-// (dv = 0).  Slot i < RMAX feeds its run accumulator and yields a flush
-// (old id, old run) when the id changes; slots >= RMAX flush every value.
-// One REDUX gives the warp-uniform set of slots with any flush.
+// One step of a lane: slots (id[i], dv[i]) of its current edge; `valid` false
+// for an empty lane (dv = 0).  Slot i < RMAX: same vertex as the run -> add;
+// else flush the run (one red) and start a new one.  Slots >= RMAX: one red.
 template <int K, int RMAX>
 __device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (&dv)[K], bool valid,
-                                              RunAcc<RMAX>& ra, int lane, double* sacc, double* ya, int H) {
-  int fv[K];
-  double fd[K];
-  unsigned lm = 0;
+                                              RunAcc<RMAX>& ra, const Sink& sk) {
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     if (i < RMAX) {
       constexpr int R1 = RMAX - 1;
       const int j = i < RMAX ? i : R1;  // compile-time after unrolling
-      const bool same = (id[i] == ra.rid[j]) | !valid;
-      fv[i] = same ? -1 : ra.rid[j];
-      fd[i] = ra.run[j];
-      ra.run[j] = same ? ra.run[j] + dv[i] : dv[i];
-      ra.rid[j] = same ? ra.rid[j] : id[i];
+      const bool fl = valid && id[i] != ra.rid[j];
+      if (fl) {
+        red_add(sk.at(ra.rid[j]), ra.run[j]);
+        ra.rid[j] = id[i];
+        ra.run[j] = 0.0;
+      }
+      ra.run[j] += dv[i];
     } else {
-      fv[i] = valid ? id[i] : -1;
-      fd[i] = dv[i];
+      if (valid) red_add(sk.at(id[i]), dv[i]);
     }
-    lm |= (fv[i] >= 0 ? 1u : 0u) << i;
-  }
-  const unsigned um = __reduce_or_sync(kFull, lm);
-  if (um) {
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-      if (um & (1u << i)) warp_flush(fv[i], fd[i], lane, sacc, ya, H);
   }
 }
 
-// EPL*32 edges of a size-K bucket: this warp's block of the staged tile,
-// one edge per lane per step.  Empty lanes read member ids of column col0
-// (valid table rows) and carry w = 0.
+// The warp's block of a staged tile (size-K bucket): lane l takes the EPL
+// consecutive columns base + l*EPL + r, r = 0..EPL-1; `cnt` = valid columns of
+// the block.  Empty lanes reuse column `base` (valid table rows) with w = 0.
 template <int N, int K, int TILE, int EPL, int RMAX>
-__device__ __forceinline__ void warp_edges(const int32_t* __restrict__ sids, const double* __restrict__ sw,
-                                           int col0, int nvalid, const double* __restrict__ xg, int gs,
-                                           RunAcc<RMAX>& ra, double* sacc, double* ya, int H, int lane) {
+__device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, const double* __restrict__ sw, int base,
+                                           int cnt, const double* __restrict__ xg, int gs, RunAcc<RMAX>& ra,
+                                           const Sink& sk, int lane) {
   constexpr int L = N - K + 1;
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
-    if (r * 32 >= nvalid) break;
-    const bool valid = r * 32 + lane < nvalid;
-    const int col = valid ? col0 + r * 32 + lane : col0;
+    const int pos = lane * EPL + r;
+    const bool valid = pos < cnt;
+    const int col = valid ? base + pos : base;
     int id[K];
     const double* rows[K];
 #pragma unroll
@@ -191,20 +165,19 @@ __device__ __forceinline__ void warp_edges(const int32_t* __restrict__ sids, con
     double dv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) dv[i] = fma(w, q[i], wF);
-    slots_deposit<K, RMAX>(id, dv, valid, ra, lane, sacc, ya, H);
+    slots_deposit<K, RMAX>(id, dv, valid, ra, sk);
   }
 }
 
 template <int N, int K, int TILE, int EPL, int RMAX>
-__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int col0, int nvalid,
-                                           const double* xg, int gs, RunAcc<RMAX>& ra, double* sacc, double* ya,
-                                           int H, int lane) {
+__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int base, int cnt,
+                                           const double* xg, int gs, RunAcc<RMAX>& ra, const Sink& sk, int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      warp_edges<N, K, TILE, EPL, RMAX>(sids, sw, col0, nvalid, xg, gs, ra, sacc, ya, H, lane);
+      warp_block<N, K, TILE, EPL, RMAX>(sids, sw, base, cnt, xg, gs, ra, sk, lane);
       return;
     }
-    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, xg, gs, ra, sacc, ya, H, lane);
+    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, base, cnt, xg, gs, ra, sk, lane);
   }
 }
 
@@ -268,24 +241,23 @@ static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* 
 }
 
 template <int TILE, int EPL>
-__device__ __forceinline__ void warp_edges_generic(int N, int k, const int32_t* sids, const double* sw, int col0,
-                                                   int nvalid, const double* xa, double* sacc, double* ya, int H,
-                                                   int lane) {
+__device__ __forceinline__ void warp_block_generic(int N, int k, const int32_t* sids, const double* sw, int base,
+                                                   int cnt, const double* xa, const Sink& sk, int lane) {
   for (int r = 0; r < EPL; ++r) {
-    const int col = col0 + r * 32 + lane;
-    const bool valid = r * 32 + lane < nvalid;
-    if (!__any_sync(kFull, valid)) break;
+    const int pos = lane * EPL + r;
+    if (pos >= cnt) break;
+    const int col = base + pos;
     int id[STTSV_MAX_RANK];
     double x[STTSV_MAX_RANK], q[STTSV_MAX_RANK];
     for (int i = 0; i < k; ++i) {
-      id[i] = valid ? sids[i * TILE + col] : -1;
-      x[i] = valid ? __ldg(xa + id[i]) : 0.0;
+      id[i] = sids[i * TILE + col];
+      x[i] = __ldg(xa + id[i]);
     }
     double F = 0.0;
     dp_edge_generic(k, N - k + 1, x, q, &F);
-    const double w = valid ? sw[col] : 0.0;
+    const double w = sw[col];
     const double wF = w * F;
-    for (int i = 0; i < k; ++i) warp_flush(id[i], fma(w, q[i], wF), lane, sacc, ya, H);
+    for (int i = 0; i < k; ++i) red_add(sk.at(id[i]), fma(w, q[i], wF));
   }
 }
 
@@ -298,14 +270,14 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   constexpr int TILE = Cfg::TILE, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX, NCW = Cfg::NCW, EPL = Cfg::EPL;
   constexpr int RMAX = Cfg::RMAX;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ] | sacc [H] f64
+  // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ]
   unsigned char* ring = smem_raw;
-  double* sacc = reinterpret_cast<double*>(smem_raw + STAGES * Cfg::STAGE_BYTES);
+  const Sink sk{p.priv + (size_t)blockIdx.x * p.H, p.ya, p.H};
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t G = gridDim.x;
+  const int64_t t_lo = p.cta_tiles[blockIdx.x], t_hi = p.cta_tiles[blockIdx.x + 1];
 
-  for (int j = tid; j < p.H; j += Cfg::THREADS) sacc[j] = 0.0;
+  for (int j = tid; j < p.H; j += Cfg::THREADS) sk.priv[j] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -315,12 +287,16 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   }
   __syncthreads();
 
+  // first bucket of this CTA's range (buckets in tile order; the index only moves forward)
+  int b0 = 0;
+  while (b0 + 1 < p.nb && t_lo >= p.b[b0 + 1].tile_begin) ++b0;
+
   if (warp == NCW) {
     // ---------------- producer warp: TMA bulk copies of tile t into stage it % STAGES
     if (lane == 0) {
+      int b = b0;
       int64_t it = 0;
-      int b = 0;
-      for (int64_t t = blockIdx.x; t < p.num_tiles; t += G, ++it) {
+      for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
         const int s = (int)(it % STAGES);
         if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
         while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
@@ -341,40 +317,48 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     RunAcc<RMAX> ra;
 #pragma unroll
     for (int i = 0; i < RMAX; ++i) {
-      ra.rid[i] = -1;
+      ra.rid[i] = 0;  // flushing (0, 0.0) is a no-op deposit
       ra.run[i] = 0.0;
     }
+    int b = b0;
     int64_t it = 0;
-    int b = 0;
-    for (int64_t t = blockIdx.x; t < p.num_tiles; t += G, ++it) {
+    for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
       const int s = (int)(it % STAGES);
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
       const int64_t m = p.b[b].m;
       const int k = p.b[b].k;
-      const int64_t e0 = (t - p.b[b].tile_begin) * TILE + warp * 32 * EPL;
+      const int base = warp * 32 * EPL;
+      const int64_t e0 = (t - p.b[b].tile_begin) * TILE + base;
       mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
       if (e0 < m) {
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
         const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
-        const int nvalid = m - e0 < 32 * EPL ? (int)(m - e0) : 32 * EPL;
-        const int col0 = warp * 32 * EPL;
+        const int cnt = m - e0 < 32 * EPL ? (int)(m - e0) : 32 * EPL;
         if constexpr (N > 0) {
-          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, col0, nvalid, p.xg, p.gs, ra, sacc, p.ya, p.H, lane);
+          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, cnt, p.xg, p.gs, ra, sk, lane);
         } else {
-          warp_edges_generic<TILE, EPL>(p.N, k, sids, sw, col0, nvalid, p.xa, sacc, p.ya, p.H, lane);
+          warp_block_generic<TILE, EPL>(p.N, k, sids, sw, base, cnt, p.xa, sk, lane);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     // flush the run accumulators
+    if (t_hi > t_lo) {
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i) warp_flush(ra.rid[i], ra.run[i], lane, sacc, p.ya, p.H);
+      for (int i = 0; i < RMAX; ++i)
+        if (ra.run[i] != 0.0) red_add(sk.at(ra.rid[i]), ra.run[i]);
+    }
   }
+  // this CTA's reds into priv are ordered before the reads below (fence + barrier);
+  // the reads go to L2 (ld.cg), where the reds were performed
+  __threadfence();
   __syncthreads();
-  for (int j = tid; j < p.H; j += Cfg::THREADS)
-    if (sacc[j] != 0.0) atomicAdd(&p.ya[j], sacc[j]);
+  for (int j = tid; j < p.H; j += Cfg::THREADS) {
+    const double v = __ldcg(sk.priv + j);
+    if (v != 0.0) red_add(p.ya + j, v);
+  }
 }
 
 }  // namespace sttsv

@@ -39,11 +39,13 @@ struct EdgeKernelParams {
   const double* xg;      // series table: row i = g[j] = x_a[i]^{j+1}/(j+1)!, j < gs (dp.cuh)
   int32_t gs;            // row stride of xg (doubles, even)
   double* ya;            // y on active vertices (accumulated)
+  double* priv;          // [grid][H] per-CTA accumulators of the hot ids (zeroed by the kernel)
   int32_t n_active;
   int32_t T;             // slots with a per-lane register run accumulator (informational)
-  int32_t H;             // ids < H: CTA shared-memory accumulators
+  int32_t H;             // ids < H accumulate in the CTA's private slice of priv
   int32_t tile_edges;    // edges per tile
-  int64_t num_tiles;     // tiles are dealt round-robin to the persistent CTAs
+  int64_t num_tiles;
+  const int64_t* cta_tiles;  // [grid+1]: CTA b processes tiles [cta_tiles[b], cta_tiles[b+1])
 };
 
 // Ranks with a fully unrolled edge kernel (one object file each); every other

@@ -112,9 +112,7 @@ EdgeKernelEntry edge_entry(int N) {
   }
 }
 
-size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int H) {
-  return e.ring_bytes + (size_t)H * sizeof(double);
-}
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int /*H*/) { return e.ring_bytes; }
 
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm) {
   cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -456,7 +456,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<double>().swap(wrow);
   std::vector<int32_t>().swap(newid);
 
-  // ---- tile order: most expensive buckets first (dynamic scheduler, LPT-like)
+  // ---- tile order: buckets most expensive first; CTAs get contiguous cost-balanced tile ranges
   int occ = 0;
   const int H = (int)std::min<int64_t>(na, 4096);
   p->ent = edge_entry(N);
@@ -500,6 +500,39 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->fma = fma;
   p->stream_bytes = ids_total * 4 + w_total * 8;
 
+  // ---- persistent grid: one contiguous range of tiles per CTA, balanced by an
+  // estimated per-edge cost (stream bytes + FP64 work + per-incidence scatter)
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int64_t grid = (int64_t)sms * std::max(occ, 1);
+  if (grid > tiles) grid = std::max<int64_t>(tiles, 1);
+  std::vector<int64_t> cta_tiles(grid + 1, tiles);
+  {
+    std::vector<double> tcost(tiles + 1, 0.0);  // prefix cost over tiles
+    int64_t t = 0;
+    for (int i = 0; i < kp.nb; ++i) {
+      const int k = kp.b[i].k;
+      const double per_edge = (4.0 * k + 8.0) + 0.5 * dp_fma(N, k) + 6.0 * k;
+      const int64_t nt = (kp.b[i].m + tile - 1) / tile;
+      for (int64_t j = 0; j < nt; ++j, ++t) {
+        const int64_t cnt = std::min<int64_t>(tile, kp.b[i].m - j * tile);
+        tcost[t + 1] = tcost[t] + per_edge * (double)cnt;
+      }
+    }
+    const double total = tcost[tiles];
+    int64_t c = 0;
+    cta_tiles[0] = 0;
+    for (int64_t b = 1; b < grid; ++b) {
+      const double target = total * (double)b / (double)grid;
+      while (c < tiles && tcost[c + 1] <= target) ++c;
+      // round to the nearer boundary
+      int64_t cut = c;
+      if (c < tiles && target - tcost[c] > tcost[c + 1] - target) cut = c + 1;
+      cta_tiles[b] = std::max(cut, cta_tiles[b - 1]);
+    }
+    cta_tiles[grid] = tiles;
+  }
+
   // ---- device memory: one allocation
   DeviceGuard g(device);
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -507,7 +540,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
                b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8);
   const int gs = series_stride(N);
   const size_t b_xg = align((size_t)na * gs * 8 + 16);
-  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg;
+  const size_t b_cta = align((size_t)(grid + 1) * 8);
+  const size_t b_priv = align((size_t)grid * H * 8 + 8);
+  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -518,10 +553,13 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->d_ya = (double*)(base + b_ids + b_w + b_act + b_xa);
   p->d_scratch = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya);
   p->d_xg = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
+  int64_t* d_cta = (int64_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg);
+  double* d_priv = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta);
   p->gs = gs;
   if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMemcpy(d_cta, cta_tiles.data(), (grid + 1) * 8, cudaMemcpyHostToDevice);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
   kp.ids = d_ids;
   kp.w = d_w;
@@ -529,11 +567,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.xg = p->d_xg;
   kp.gs = gs;
   kp.ya = p->d_ya;
+  kp.cta_tiles = d_cta;
+  kp.priv = d_priv;
 
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  int64_t grid = (int64_t)sms * std::max(occ, 1);
-  if (grid > tiles) grid = std::max<int64_t>(tiles, 1);
   p->grid = (int)grid;
   p->block = p->ent.block;
   *out = p;
