@@ -42,16 +42,35 @@ namespace sttsv {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Prefix memoisation along a lane's consecutive edges (dp.cuh dp_core, h > 0);
+// compile-time switch for A/B timing (0 = recompute every prefix).
+#ifndef STTSV_MEMO
+#define STTSV_MEMO 0
+#endif
+// Register-lean DP (dp.cuh dp_edge_lean): rows re-read in the suffix pass.
+#ifndef STTSV_LEAN
+#define STTSV_LEAN 0
+#endif
+
 template <int N>
 struct EdgeCfg {
   static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
-  static constexpr int EPL = 5;                             // consecutive edges per lane per tile (odd)
+#ifndef STTSV_EPL
+#define STTSV_EPL 5
+#endif
+#ifndef STTSV_RING_KB
+#define STTSV_RING_KB 220
+#endif
+  static constexpr int EPL = STTSV_EPL;                     // consecutive edges per lane per tile (odd)
   static constexpr int EDGE_BYTES = 4 * KMAX + 8;           // staged bytes per edge (ids + w')
-  static constexpr int RING_BUDGET = 220 * 1024;            // dynamic shared memory (<= 227 KB)
+  static constexpr int RING_BUDGET = STTSV_RING_KB * 1024;  // dynamic shared memory (<= 227 KB)
   // consumer warps: 15 (+1 producer = 4 warps per SMSP) for small ranks; fewer
   // when two stages of the largest bucket would not fit the ring budget
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
-  static constexpr int NCW_PREF = (N >= 1 && N <= 10) ? 15 : 7;
+#ifndef STTSV_NCW_SMALL
+#define STTSV_NCW_SMALL 15
+#endif
+  static constexpr int NCW_PREF = (N >= 1 && N <= 10) ? STTSV_NCW_SMALL : 7;
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
@@ -60,6 +79,10 @@ struct EdgeCfg {
   static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
   static constexpr int RMAX = KMAX < 8 ? KMAX : 8;          // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = 1;
+#ifndef STTSV_PF
+#define STTSV_PF 2
+#endif
+  static constexpr int PF = STTSV_PF;                       // L2 prefetch distance (tiles)
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
 };
@@ -96,6 +119,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// L2 prefetch of a global range (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------ scatter
 struct Sink {
   double* priv;  // this CTA's private slice for ids < H
@@ -107,77 +135,93 @@ struct Sink {
 __device__ __forceinline__ void red_add(double* a, double d) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(d) : "memory");
 }
-
 template <int RMAX>
 struct RunAcc {
   int rid[RMAX];
   double run[RMAX];
 };
 
-// One step of a lane: slots (id[i], dv[i]) of its current edge; `valid` false
-// for an empty lane (dv = 0).  Slot i < RMAX: same vertex as the run -> add;
-// else flush the run (one red) and start a new one.  Slots >= RMAX: one red.
+// One step of a lane: slots (id[i], dv[i]) of its current edge.  Slot i <
+// RMAX: same vertex as the run -> add; else flush the run (one red) and start
+// a new one.  Slots >= RMAX: one red.
 template <int K, int RMAX>
-__device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (&dv)[K], bool valid,
-                                              RunAcc<RMAX>& ra, const Sink& sk) {
+__device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (&dv)[K], RunAcc<RMAX>& ra,
+                                              const Sink& sk) {
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     if (i < RMAX) {
       constexpr int R1 = RMAX - 1;
       const int j = i < RMAX ? i : R1;  // compile-time after unrolling
-      const bool fl = valid && id[i] != ra.rid[j];
-      if (fl) {
+      const bool fl = id[i] != ra.rid[j];
+      if (fl) {  // rare: a branch (computing the address every step costs more)
         red_add(sk.at(ra.rid[j]), ra.run[j]);
         ra.rid[j] = id[i];
         ra.run[j] = 0.0;
       }
       ra.run[j] += dv[i];
     } else {
-      if (valid) red_add(sk.at(id[i]), dv[i]);
+      red_add(sk.at(id[i]), dv[i]);
     }
   }
 }
 
 // The warp's block of a staged tile (size-K bucket): lane l takes the EPL
-// consecutive columns base + l*EPL + r, r = 0..EPL-1; `cnt` = valid columns of
-// the block.  Empty lanes reuse column `base` (valid table rows) with w = 0.
+// consecutive columns base + l*EPL + r, r = 0..EPL-1.  Buckets are padded to
+// whole tiles with weight-0 copies of their last edge, so every column is valid.
 template <int N, int K, int TILE, int EPL, int RMAX>
 __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, const double* __restrict__ sw, int base,
-                                           int cnt, const double* __restrict__ xg, int gs, RunAcc<RMAX>& ra,
-                                           const Sink& sk, int lane) {
+                                           const double* __restrict__ xg, RunAcc<RMAX>& ra, const Sink& sk,
+                                           int lane) {
   constexpr int L = N - K + 1;
+  constexpr int KP = K > 2 ? K - 2 : 1;
+  constexpr int GS = series_stride(N);
+  double P[KP][L];  // prefix products, kept between this lane's consecutive edges
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
-    const int pos = lane * EPL + r;
-    const bool valid = pos < cnt;
-    const int col = valid ? base + pos : base;
+    const int col = base + lane * EPL + r;
     int id[K];
     const double* rows[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       id[i] = sids[i * TILE + col];
-      rows[i] = xg + (size_t)id[i] * gs;
+      rows[i] = xg + id[i] * GS;  // GS compile-time: one IMAD.WIDE
     }
-    const double w = valid ? sw[col] : 0.0;
+    // shared leading members with this lane's previous edge (the run ids hold
+    // it); warp minimum, 0 on a tile's first step
+    int h = 0;
+    if constexpr (K > 3 && STTSV_MEMO) {
+      if (r > 0) {
+        int hl = 0;
+#pragma unroll
+        for (int i = 0; i < K - 3 && i < RMAX; ++i)
+          if (hl == i && id[i] == ra.rid[i]) hl = i + 1;
+        h = __reduce_min_sync(kFull, hl);
+      }
+    }
+    const double w = sw[col];
     double q[K], F;
-    dp_edge_table<K, L>(rows, q, F);
+#if STTSV_LEAN
+    dp_edge_lean<K, L>(rows, q, F);
+#else
+    dp_edge_table<K, L>(rows, P, STTSV_MEMO ? h : 0, q, F);
+#endif
     const double wF = w * F;
     double dv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) dv[i] = fma(w, q[i], wF);
-    slots_deposit<K, RMAX>(id, dv, valid, ra, sk);
+    slots_deposit<K, RMAX>(id, dv, ra, sk);
   }
 }
 
 template <int N, int K, int TILE, int EPL, int RMAX>
-__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int base, int cnt,
-                                           const double* xg, int gs, RunAcc<RMAX>& ra, const Sink& sk, int lane) {
+__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int base,
+                                           const double* xg, RunAcc<RMAX>& ra, const Sink& sk, int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      warp_block<N, K, TILE, EPL, RMAX>(sids, sw, base, cnt, xg, gs, ra, sk, lane);
+      warp_block<N, K, TILE, EPL, RMAX>(sids, sw, base, xg, ra, sk, lane);
       return;
     }
-    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, base, cnt, xg, gs, ra, sk, lane);
+    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, base, xg, ra, sk, lane);
   }
 }
 
@@ -242,11 +286,9 @@ static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* 
 
 template <int TILE, int EPL>
 __device__ __forceinline__ void warp_block_generic(int N, int k, const int32_t* sids, const double* sw, int base,
-                                                   int cnt, const double* xa, const Sink& sk, int lane) {
+                                                   const double* xa, const Sink& sk, int lane) {
   for (int r = 0; r < EPL; ++r) {
-    const int pos = lane * EPL + r;
-    if (pos >= cnt) break;
-    const int col = base + pos;
+    const int col = base + lane * EPL + r;
     int id[STTSV_MAX_RANK];
     double x[STTSV_MAX_RANK], q[STTSV_MAX_RANK];
     for (int i = 0; i < k; ++i) {
@@ -292,19 +334,29 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   while (b0 + 1 < p.nb && t_lo >= p.b[b0 + 1].tile_begin) ++b0;
 
   if (warp == NCW) {
-    // ---------------- producer warp: TMA bulk copies of tile t into stage it % STAGES
+    // ---------------- producer warp: TMA bulk copies of tile t into stage it % STAGES,
+    // plus an L2 prefetch of tile t + PF (hides HBM latency beyond the ring's depth)
     if (lane == 0) {
-      int b = b0;
+      int b = b0, bp = b0;
       int64_t it = 0;
       for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
         const int s = (int)(it % STAGES);
+        if constexpr (Cfg::PF > 0) {
+          const int64_t tp = t + Cfg::PF;
+          if (tp < t_hi) {
+            while (bp + 1 < p.nb && tp >= p.b[bp + 1].tile_begin) ++bp;
+            const BucketDesc& bd = p.b[bp];
+            const int64_t e0 = (tp - bd.tile_begin) * TILE;
+            constexpr uint32_t id_bytes = TILE * 4, w_bytes = TILE * 8;
+            for (int i = 0; i < bd.k; ++i) bulk_prefetch_l2(p.ids + bd.ids_off + i * bd.stride + e0, id_bytes);
+            bulk_prefetch_l2(p.w + bd.w_off + e0, w_bytes);
+          }
+        }
         if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
         while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const BucketDesc& bd = p.b[b];
-        const int64_t e0 = (t - bd.tile_begin) * TILE;
-        const int64_t cnt = bd.m - e0 < TILE ? bd.m - e0 : TILE;
-        const uint32_t id_bytes = (uint32_t)(((cnt + 3) & ~3LL) * 4);
-        const uint32_t w_bytes = (uint32_t)(((cnt + 1) & ~1LL) * 8);
+        const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
+        constexpr uint32_t id_bytes = TILE * 4, w_bytes = TILE * 8;
         unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], id_bytes * bd.k + w_bytes);
         for (int i = 0; i < bd.k; ++i)
@@ -325,20 +377,17 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
       const int s = (int)(it % STAGES);
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
-      const int64_t m = p.b[b].m;
       const int k = p.b[b].k;
       const int base = warp * 32 * EPL;
-      const int64_t e0 = (t - p.b[b].tile_begin) * TILE + base;
       mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
-      if (e0 < m) {
+      {
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
         const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
-        const int cnt = m - e0 < 32 * EPL ? (int)(m - e0) : 32 * EPL;
         if constexpr (N > 0) {
-          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, cnt, p.xg, p.gs, ra, sk, lane);
+          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, p.xg, ra, sk, lane);
         } else {
-          warp_block_generic<TILE, EPL>(p.N, k, sids, sw, base, cnt, p.xa, sk, lane);
+          warp_block_generic<TILE, EPL>(p.N, k, sids, sw, base, p.xa, sk, lane);
         }
       }
       __syncwarp();

@@ -16,7 +16,7 @@ struct BucketDesc {
   int32_t k;
   int32_t pad_;
   int64_t m;           // edges in this bucket (this shard)
-  int64_t stride;      // column stride of ids (>= m, multiple of 4)
+  int64_t stride;      // column stride of ids: m padded to whole tiles (weight-0 copies of the last edge)
   int64_t tile_begin;  // first tile of this bucket in the kernel's tile order
   int64_t ids_off;     // element offset of column 0 in the ids pool
   int64_t w_off;       // element offset in the weight pool

@@ -381,11 +381,13 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   // ---- buckets and this shard's slices
   std::vector<int64_t> pos, count;
   bucket_positions(m, sizes, N, pos, count);
+  p->ent = edge_entry(N);
+  const int tile = p->ent.tile;
   std::vector<int64_t> lo(N + 1), mk(N + 1, 0), stride(N + 1, 0);
   for (int k = 1; k <= N; ++k) {
     lo[k] = bucket_lo(count[k], world, rank);
     mk[k] = bucket_lo(count[k], world, rank + 1) - lo[k];
-    stride[k] = (mk[k] + 3) & ~(int64_t)3;
+    stride[k] = (mk[k] + tile - 1) / tile * tile;  // padded to whole tiles (see below)
     p->edges_per_size[k] = mk[k];
     p->local_edges += mk[k];
     p->local_inc += mk[k] * k;
@@ -451,6 +453,13 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = src[i];
       h_w[w_off[k] + j] = wrow[w_off[k] + perm[j]];
     }
+    // pad the bucket to whole tiles with copies of its last edge at weight 0:
+    // the kernel then never meets a partial tile (no per-lane validity tests),
+    // a padded edge contributes exactly 0 and continues the last edge's runs
+    for (int64_t j = mk[k]; j < st; ++j) {
+      for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = col[(int64_t)i * st + mk[k] - 1];
+      h_w[w_off[k] + j] = 0.0;
+    }
   }
   std::vector<int32_t>().swap(rows);
   std::vector<double>().swap(wrow);
@@ -459,9 +468,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   // ---- tile order: buckets most expensive first; CTAs get contiguous cost-balanced tile ranges
   int occ = 0;
   const int H = (int)std::min<int64_t>(na, 4096);
-  p->ent = edge_entry(N);
   const int T = p->ent.run_slots;
-  const int tile = p->ent.tile;
   {
     DeviceGuard g(device);
     cudaError_t e0 = cudaSetDevice(device);
@@ -489,7 +496,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     b.tile_begin = tiles;
     b.ids_off = ids_off[k];
     b.w_off = w_off[k];
-    tiles += (mk[k] + tile - 1) / tile;
+    tiles += stride[k] / tile;
     fma += dp_fma(N, k) * (double)mk[k];
   }
   kp.num_tiles = tiles;

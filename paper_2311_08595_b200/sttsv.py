@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsttsv.so")
+LIB_PATH = os.environ.get("STTSV_LIB_PATH") or os.path.join(_HERE, "libsttsv.so")
 MAX_RANK = 32
 
 STTSV_CANONICALIZE = 1 << 0

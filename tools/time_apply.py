@@ -1,0 +1,38 @@
+"""Time sttsv_apply on one config (CUDA events, edge-kernel events from the
+library), for A/B comparisons of library variants (STTSV_LIB_PATH).
+
+  python tools/time_apply.py [config] [reps]
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2311_08595_b200 as S  # noqa: E402
+import workloads as W  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "large"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+hg = W.generate(name)
+plan = S.Plan.from_hypergraph(hg)
+x = torch.from_numpy(hg.x).cuda()
+y = torch.empty_like(x)
+for _ in range(3):
+    plan.apply(x, y)
+torch.cuda.synchronize()
+ref = y.clone()
+plan.profile(True)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(reps):
+    plan.apply(x, y)
+e1.record()
+torch.cuda.synchronize()
+kms, kn = plan.profile_read()
+err = float(((y - ref).abs().max() / ref.abs().max()).item())
+print("%s lib=%s step_ms=%.4f kernel_ms=%.4f rerun_rel_diff=%.2e" % (
+    name, os.path.basename(os.environ.get("STTSV_LIB_PATH", "libsttsv.so")), e0.elapsed_time(e1) / reps,
+    kms / kn, err), flush=True)

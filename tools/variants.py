@@ -1,0 +1,30 @@
+"""Build experimental variants of libsttsv.so that differ only in the rank-N
+edge-kernel object (compile-time knobs), for A/B timing on one GPU call.
+
+  python tools/variants.py N NAME:-DFLAG=1,-DOTHER=2 NAME2:...   -> build/variants/libsttsv_NAME.so
+  STTSV_LIB_PATH=build/variants/libsttsv_NAME.so python tools/time_apply.py large
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2311_08595_b200 import build as B  # noqa: E402
+
+N = int(sys.argv[1])
+B.build()
+out = os.path.join(ROOT, "build", "variants")
+os.makedirs(out, exist_ok=True)
+objs = [os.path.join(B.OBJ, "edge_n%d.o" % n) for n in B.compiled_ranks() + [0] if n != N]
+objs += [os.path.join(B.OBJ, "kernels.o"), os.path.join(B.OBJ, "plan.o")]
+for spec in sys.argv[2:]:
+    name, _, flags = spec.partition(":")
+    flags = [f for f in flags.split(",") if f]
+    o = os.path.join(out, "edge_n%d_%s.o" % (N, name))
+    subprocess.check_call([B.NVCC] + B.NVFLAGS + flags + ["-DSTTSV_INST_N=%d" % N, "-c",
+                           os.path.join(B.CSRC, "edge_inst.cu"), "-o", o])
+    lib = os.path.join(out, "libsttsv_%s.so" % name)
+    subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib, o] + objs +
+                          ["-ldl", "-lgomp"])
+    print(lib)
