@@ -42,8 +42,10 @@ __device__ __forceinline__ void series_row(double x, double* __restrict__ g, int
   }
 }
 
-// load coefficients 0..L-1 of one table row with 16-byte loads (rows are 16-B
-// aligned with an even stride >= L, so an odd L reads one padding coefficient)
+// load coefficients 0..L-1 of one table row with 128-bit loads (rows are 32-B
+// aligned with a stride that is a multiple of 4 and >= L, so an odd L reads one
+// unused coefficient inside the row).  (256-bit LDG.E.ENL2.256 loads measured
+// 1.4x slower on the edge kernel.)
 template <int L>
 __device__ __forceinline__ void load_series(const double* __restrict__ row, double (&g)[L]) {
   const double2* r2 = reinterpret_cast<const double2*>(row);

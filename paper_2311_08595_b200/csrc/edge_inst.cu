@@ -22,3 +22,14 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   return e;
 }
 }  // namespace sttsv
+
+#if STTSV_WAITPROF
+extern "C" int sttsv_debug_wait(unsigned long long out[4], int reset) {
+  cudaMemcpyFromSymbol(out, sttsv::g_wait_cycles, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(sttsv::g_wait_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -42,6 +42,15 @@ namespace sttsv {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Debug instrumentation (compile with -DSTTSV_WAITPROF=1): consumer warps add the
+// cycles they spend waiting on `full` barriers and their total cycles.
+#ifndef STTSV_WAITPROF
+#define STTSV_WAITPROF 0
+#endif
+#if STTSV_WAITPROF
+__device__ unsigned long long g_wait_cycles[4];
+#endif
+
 // Prefix memoisation along a lane's consecutive edges (dp.cuh dp_core, h > 0);
 // compile-time switch for A/B timing (0 = recompute every prefix).
 #ifndef STTSV_MEMO
@@ -184,7 +193,7 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       id[i] = sids[i * TILE + col];
-      rows[i] = xg + id[i] * GS;  // GS compile-time: one IMAD.WIDE
+      rows[i] = xg + (size_t)(uint32_t)id[i] * GS;  // GS compile-time: one IMAD.WIDE.U32
     }
     // shared leading members with this lane's previous edge (the run ids hold
     // it); warp minimum, 0 on a tile's first step
@@ -374,12 +383,22 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     }
     int b = b0;
     int64_t it = 0;
+#if STTSV_WAITPROF
+    long long wait_cyc = 0;
+    const long long c_start = clock64();
+#endif
     for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
       const int s = (int)(it % STAGES);
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
       const int k = p.b[b].k;
       const int base = warp * 32 * EPL;
+#if STTSV_WAITPROF
+      const long long w0 = clock64();
       mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      wait_cyc += clock64() - w0;
+#else
+      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+#endif
       {
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
@@ -393,6 +412,13 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+#if STTSV_WAITPROF
+    if (lane == 0) {
+      atomicAdd(&g_wait_cycles[0], (unsigned long long)wait_cyc);
+      atomicAdd(&g_wait_cycles[1], (unsigned long long)(clock64() - c_start));
+      atomicAdd(&g_wait_cycles[2], 1ull);
+    }
+#endif
     // flush the run accumulators
     if (t_hi > t_lo) {
 #pragma unroll

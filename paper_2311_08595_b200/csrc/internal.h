@@ -26,8 +26,8 @@ constexpr int kMaxBuckets = STTSV_MAX_RANK;
 
 // Row stride (doubles) of the per-apply series table x_g (dp.cuh): coefficients
 // j = 0..N-2 are used (L - 1 <= N - 2 for k >= 2; the singleton needs j = N - 2),
-// padded to an even count so rows are 16-byte aligned.
-__host__ __device__ constexpr int series_stride(int N) { return N < 2 ? 2 : ((N - 1 + 1) & ~1); }
+// padded to a multiple of 4 so rows are 32-byte aligned (256-bit loads).
+__host__ __device__ constexpr int series_stride(int N) { return N < 2 ? 4 : ((N - 1 + 3) & ~3); }
 
 struct EdgeKernelParams {
   int32_t N;             // rank

@@ -33,6 +33,13 @@ e1.record()
 torch.cuda.synchronize()
 kms, kn = plan.profile_read()
 err = float(((y - ref).abs().max() / ref.abs().max()).item())
+lib = S.load()
+if hasattr(lib, "sttsv_debug_wait"):
+    import ctypes
+    buf = (ctypes.c_ulonglong * 4)()
+    lib.sttsv_debug_wait(buf, 1)
+    print("  consumer full-barrier wait: %.1f%% of consumer cycles (%d warp samples)" % (
+        100.0 * buf[0] / max(buf[1], 1), buf[2]))
 print("%s lib=%s step_ms=%.4f kernel_ms=%.4f rerun_rel_diff=%.2e" % (
     name, os.path.basename(os.environ.get("STTSV_LIB_PATH", "libsttsv.so")), e0.elapsed_time(e1) / reps,
     kms / kn, err), flush=True)
