@@ -1,0 +1,118 @@
+"""Per-config measurements on one GPU (all five BASELINE.json configs).
+
+  python tools/bench_configs.py [--configs tiny,mid,...] [--reps 20] [--out file.jsonl]
+
+For each config: plan build time, one-apply event time (median of reps),
+edge-kernel time (library events), incidences/s, the edge kernel's
+algorithmic HBM GB/s and FP64 TFLOP/s against the measured peaks, and, for
+tiny/mid (launch-bound), the throughput of 100 applies captured in one CUDA
+graph.  `centrality` additionally times sttsv_power_iterate(50) (A14).
+Inputs resident in HBM; every config's edge stream except tiny/mid exceeds
+nothing in particular — the numbers are device time, not end to end.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2311_08595_b200 as S  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def ev_time(fn, reps, stream):
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), min(ts)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="tiny,mid,high-rank,large,centrality")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    hbm, hbm_src = bench.measured_peaks()
+    fp64, fp64_src = bench.fp64_peak_tflops()
+    stream = torch.cuda.current_stream()
+    out = open(args.out, "a") if args.out else None
+    for name in args.configs.split(","):
+        hg = W.generate(name)
+        t0 = time.perf_counter()
+        plan = S.Plan.from_hypergraph(hg)
+        t_plan = time.perf_counter() - t0
+        info = plan.info()
+        x = torch.from_numpy(hg.x).cuda()
+        y = torch.empty_like(x)
+        for _ in range(3):
+            plan.apply(x, y)
+        torch.cuda.synchronize()
+        plan.profile(True)
+        med, mn = ev_time(lambda: plan.apply(x, y), args.reps, stream)
+        kms, kn = plan.profile_read()
+        plan.profile(False)
+        kavg = kms / max(kn, 1)
+        alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
+        rec = {"config": name, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank, "incidences": hg.incidences,
+               "n_active": info["n_active"], "plan_s": round(t_plan, 2),
+               "apply_ms_median": med, "apply_ms_min": mn, "edge_kernel_ms": kavg,
+               "incidences_per_s": hg.incidences / (med * 1e-3),
+               "edge_kernel_hbm_gbs": alg_bytes / (kavg * 1e-3) / 1e9,
+               "edge_kernel_hbm_frac": alg_bytes / (kavg * 1e-3) / 1e9 / hbm,
+               "edge_kernel_fp64_tflops": 2 * info["fma_per_apply"] / (kavg * 1e-3) / 1e12,
+               "edge_kernel_fp64_frac": 2 * info["fma_per_apply"] / (kavg * 1e-3) / 1e12 / fp64,
+               "alg_bytes": alg_bytes, "fma_per_apply": info["fma_per_apply"],
+               "peaks": {"hbm_gbs": hbm, "hbm_src": hbm_src, "fp64_tflops": fp64, "fp64_src": fp64_src}}
+        if name in ("tiny", "mid"):
+            g = torch.cuda.CUDAGraph()
+            s2 = torch.cuda.Stream()
+            s2.wait_stream(stream)
+            with torch.cuda.stream(s2):
+                plan.apply(x, y, s2)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=s2):
+                    for _ in range(100):
+                        plan.apply(x, y, s2)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            gmed, _ = ev_time(g.replay, 10, stream)
+            rec["graph100_ms_per_apply"] = gmed / 100
+            rec["graph100_incidences_per_s"] = hg.incidences / (gmed / 100 * 1e-3)
+        if name == "centrality":
+            x0 = torch.full((hg.n,), 1.0 / hg.n, dtype=torch.float64, device="cuda")
+            xx = x0.clone()
+            z = torch.empty_like(x0)
+
+            def pi():
+                xx.copy_(x0)
+                plan.power_iterate(xx, 50, z)
+            pi()
+            med50, _ = ev_time(pi, 3, stream)
+            rec["power50_ms"] = med50
+            rec["power50_ms_per_iter"] = med50 / 50
+            rec["power50_incidences_per_s"] = 50 * hg.incidences / (med50 * 1e-3)
+        line = json.dumps(rec)
+        print(line, flush=True)
+        if out:
+            out.write(line + "\n")
+        plan.close()
+        del plan, x, y, hg
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

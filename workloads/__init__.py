@@ -136,8 +136,12 @@ class Hypergraph:
         sizes = self.sizes[edge_ids]
         offsets = np.zeros(len(edge_ids) + 1, dtype=np.int64)
         np.cumsum(sizes, out=offsets[1:])
-        idx = np.concatenate([self.edge(int(e)) for e in edge_ids]) if len(edge_ids) else \
-            np.zeros(0, dtype=np.int32)
+        if len(edge_ids):
+            starts = self.offsets[edge_ids]
+            rel = np.arange(int(offsets[-1]), dtype=np.int64) - np.repeat(offsets[:-1], sizes)
+            idx = self.indices[np.repeat(starts, sizes) + rel]
+        else:
+            idx = np.zeros(0, dtype=np.int32)
         return Hypergraph(self.n, self.rank, sizes.astype(np.int32), offsets, idx.astype(np.int32),
                           self.weights[edge_ids].copy(), self.x, self.config, dict(self.meta))
 
