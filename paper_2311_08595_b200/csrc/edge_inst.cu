@@ -18,7 +18,9 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.tile = EdgeCfg<STTSV_INST_N>::TILE;
   e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::STAGES * EdgeCfg<STTSV_INST_N>::STAGE_BYTES;
   e.rank = STTSV_INST_N;
-  e.run_slots = STTSV_INST_N > 0 ? EdgeCfg<STTSV_INST_N>::RMAX : 0;
+  e.run_slots = EdgeCfg<STTSV_INST_N>::RMAX;
+  e.big = EdgeCfg<STTSV_INST_N>::BIG ? (STTSV_BIG_LOCAL ? 2 : 1) : 0;
+  e.consumers = 32 * EdgeCfg<STTSV_INST_N>::NCW;
   return e;
 }
 }  // namespace sttsv

@@ -61,40 +61,69 @@ __device__ unsigned long long g_wait_cycles[4];
 #define STTSV_LEAN 0
 #endif
 
-template <int N>
-struct EdgeCfg {
-  static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
 #ifndef STTSV_EPL
 #define STTSV_EPL 5
 #endif
 #ifndef STTSV_RING_KB
 #define STTSV_RING_KB 220
 #endif
-  static constexpr int EPL = STTSV_EPL;                     // consecutive edges per lane per tile (odd)
-  static constexpr int EDGE_BYTES = 4 * KMAX + 8;           // staged bytes per edge (ids + w')
-  static constexpr int RING_BUDGET = STTSV_RING_KB * 1024;  // dynamic shared memory (<= 227 KB)
-  // consumer warps: 15 (+1 producer = 4 warps per SMSP) for small ranks; fewer
-  // when two stages of the largest bucket would not fit the ring budget
-  static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
 #ifndef STTSV_NCW_SMALL
 #define STTSV_NCW_SMALL 15
 #endif
-  static constexpr int NCW_PREF = (N >= 1 && N <= 10) ? STTSV_NCW_SMALL : 7;
+#ifndef STTSV_PF
+#define STTSV_PF 2
+#endif
+// ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
+// path: runtime member loop, prefix stack in shared memory (edge_big below)
+#ifndef STTSV_BIG_MIN
+#define STTSV_BIG_MIN 13
+#endif
+// 1: the large-rank prefix stack is a per-thread local-memory array (L1-cached)
+// instead of shared memory, which allows more consumer warps
+#ifndef STTSV_BIG_LOCAL
+#define STTSV_BIG_LOCAL 1
+#endif
+#ifndef STTSV_BIG_NCW
+#define STTSV_BIG_NCW 11
+#endif
+
+template <int N>
+struct EdgeCfg {
+  static constexpr bool BIG = (N == 0) || (N >= STTSV_BIG_MIN);
+  static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
+  static constexpr int EPL = BIG ? 1 : STTSV_EPL;           // consecutive edges per lane per tile (odd)
+  static constexpr int EDGE_BYTES = 4 * KMAX + 8;           // staged bytes per edge (ids + w')
+  // dynamic shared memory for the TMA ring (<= 227 KB in total; the large-rank
+  // path also needs its prefix stack)
+  static constexpr int RING_BUDGET = BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024 : STTSV_RING_KB * 1024;
+  // consumer warps: 15 (+1 producer = 4 warps per SMSP) for small ranks; fewer
+  // when two stages of the largest bucket would not fit the ring budget; the
+  // large-rank path runs 4 (2 for the generic kernel) register-heavy warps
+  static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
+  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 10 ? STTSV_NCW_SMALL : 7);
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
   static constexpr int STAGE_BYTES = TILE * EDGE_BYTES;
   static constexpr int STAGES_FIT = RING_BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
-  static constexpr int RMAX = KMAX < 8 ? KMAX : 8;          // slots with a register run accumulator
-  static constexpr int MIN_BLOCKS = 1;
-#ifndef STTSV_PF
-#define STTSV_PF 2
+  static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
+#ifndef STTSV_MIN_BLOCKS
+#define STTSV_MIN_BLOCKS 1
 #endif
+  static constexpr int MIN_BLOCKS = BIG ? 1 : STTSV_MIN_BLOCKS;
   static constexpr int PF = STTSV_PF;                       // L2 prefetch distance (tiles)
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
 };
+
+// doubles of prefix stack one consumer thread of the large-rank path needs for
+// rank N: rows P_0..P_{K-4} of length L = N-K+1, maximised over K
+__host__ __device__ constexpr int big_stack_doubles(int N) {
+  int m = 0;
+  for (int K = 4; K <= N; ++K) m = (K - 3) * (N - K + 1) > m ? (K - 3) * (N - K + 1) : m;
+  return m;
+}
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -115,6 +144,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+// producer-side wait: back off between polls so the spinning warp does not
+// steal issue slots from the consumers
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(256);
+  }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -234,81 +279,118 @@ __device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const dou
   }
 }
 
-// ---------------------------------------------------------------- generic
-// Runtime (K, L) DP for ranks without a compiled specialisation: same
-// recurrence as dp_edge, arrays in local memory.  Returns q_i = Q_i[D] and F = F[D-1].
-static __device__ __noinline__ void dp_edge_generic(int K, int L, const double* x, double* q, double* Fout) {
-  const int D = L - 1;
-  double g[STTSV_MAX_RANK][STTSV_MAX_RANK];
-  for (int i = 0; i < K; ++i) {
-    double pw = x[i], f = 1.0;
-    g[i][0] = pw;
-    for (int j = 1; j < L; ++j) {
-      pw *= x[i];
-      f *= double(j + 1);
-      g[i][j] = pw / f;
-    }
+// ------------------------------------------------------- large-rank path
+// For large L = N-K+1 a lane cannot hold K series in registers.  One edge per
+// lane; members are walked by a RUNTIME loop; the working rows (current prefix
+// P, one member row g, suffix S) are L-long register arrays; the prefix stack
+// P_0..P_{K-4} lives in shared memory (thread-interleaved: conflict-free), and
+// each member's series row is (re)loaded from the L1/L2-resident table where
+// it is used.  Products are formed in place (descending coefficient order).
+
+// a = (a*b) mod t^L, in place
+template <int L>
+__device__ __forceinline__ void trunc_mul_inplace(double (&a)[L], const double (&b)[L]) {
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j) {
+    double s = a[0] * b[j];
+#pragma unroll
+    for (int i = 1; i <= j; ++i) s = fma(a[i], b[j - i], s);
+    a[j] = s;
   }
-  if (K == 1) {
-    // q = [t^D] (empty product) = [D == 0];  F = [t^{D-1}] g_0 = x^D / D!
-    q[0] = D == 0 ? 1.0 : 0.0;
-    *Fout = D >= 1 ? g[0][D - 1] : 0.0;
-    return;
-  }
-  auto coefD = [&](const double* a, const double* b, int deg) {
-    double s = a[0] * b[deg];
-    for (int j = 1; j <= deg; ++j) s = fma(a[j], b[deg - j], s);
-    return s;
-  };
-  auto tmul = [&](const double* a, const double* b, double* r) {
-    for (int j = 0; j < L; ++j) {
-      double s = a[0] * b[j];
-      for (int i = 1; i <= j; ++i) s = fma(a[i], b[j - i], s);
-      r[j] = s;
-    }
-  };
-  if (K == 2) {
-    *Fout = D >= 1 ? coefD(g[0], g[1], D - 1) : 0.0;
-    q[0] = g[1][D];
-    q[1] = g[0][D];
-    return;
-  }
-  double P[STTSV_MAX_RANK][STTSV_MAX_RANK];
-  for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
-  for (int i = 1; i <= K - 3; ++i) tmul(P[i - 1], g[i], P[i]);
-  q[K - 1] = coefD(P[K - 3], g[K - 2], D);
-  q[K - 2] = coefD(P[K - 3], g[K - 1], D);
-  double S[STTSV_MAX_RANK], T[STTSV_MAX_RANK];
-  tmul(g[K - 2], g[K - 1], S);
-  *Fout = D >= 1 ? coefD(P[K - 3], S, D - 1) : 0.0;
-  for (int i = K - 3; i >= 1; --i) {
-    q[i] = coefD(P[i - 1], S, D);
-    if (i > 1) {
-      tmul(g[i], S, T);
-      for (int j = 0; j < L; ++j) S[j] = T[j];
-    } else {
-      q[0] = coefD(g[1], S, D);
-    }
-  }
-  if (K == 3) q[0] = S[D];
 }
 
-template <int TILE, int EPL>
-__device__ __forceinline__ void warp_block_generic(int N, int k, const int32_t* sids, const double* sw, int base,
-                                                   const double* xa, const Sink& sk, int lane) {
-  for (int r = 0; r < EPL; ++r) {
-    const int col = base + lane * EPL + r;
-    int id[STTSV_MAX_RANK];
-    double x[STTSV_MAX_RANK], q[STTSV_MAX_RANK];
-    for (int i = 0; i < k; ++i) {
-      id[i] = sids[i * TILE + col];
-      x[i] = __ldg(xa + id[i]);
+// deposit of slot i (warp-uniform runtime index): slots < RB use the run
+// accumulators (compile-time register index via a uniform compare chain)
+template <int RB>
+__device__ __forceinline__ void dep_slot(int i, int v, double d, RunAcc<RB>& ra, const Sink& sk) {
+  if (i < RB) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (i == r) {
+        if (v != ra.rid[r]) {
+          red_add(sk.at(ra.rid[r]), ra.run[r]);
+          ra.rid[r] = v;
+          ra.run[r] = 0.0;
+        }
+        ra.run[r] += d;
+      }
     }
+  } else {
+    red_add(sk.at(v), d);
+  }
+}
+
+// one edge of size K (runtime) with L = N-K+1 (compile time); sid = member 0's
+// id in the staged tile (member i at sid[i * TILE]); stk = this thread's stack
+// (row r coefficient j at stk[(r * L + j) * NT])
+template <int L, int TILE, int NT, int RB>
+__device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid, double w,
+                                         const double* __restrict__ xg, int gs, double* __restrict__ stk,
+                                         RunAcc<RB>& ra, const Sink& sk) {
+  // NT = 1: stk is a thread-private (local) array; else thread-interleaved shared memory
+  constexpr int D = L - 1;
+  auto row = [&](int i) { return xg + (size_t)(uint32_t)sid[i * TILE] * gs; };
+  if (K == 1) {
+    // singleton: Q = 1 (empty product), F = g_0:  q = [D == 0],  F[D-1] = x^D / D!
+    const double F = D >= 1 ? __ldg(row(0) + (D >= 1 ? D - 1 : 0)) : 0.0;
+    dep_slot<RB>(0, sid[0], w * ((D == 0 ? 1.0 : 0.0) + F), ra, sk);
+    return;
+  }
+  if (K == 2) {
+    double a[L], b[L];
+    load_series<L>(row(0), a);
+    load_series<L>(row(1), b);
     double F = 0.0;
-    dp_edge_generic(k, N - k + 1, x, q, &F);
-    const double w = sw[col];
+    if constexpr (D >= 1) F = coef<D - 1, L>(a, b);
     const double wF = w * F;
-    for (int i = 0; i < k; ++i) red_add(sk.at(id[i]), fma(w, q[i], wF));
+    dep_slot<RB>(0, sid[0], fma(w, b[D], wF), ra, sk);
+    dep_slot<RB>(1, sid[TILE], fma(w, a[D], wF), ra, sk);
+    return;
+  }
+  double cur[L], g[L], S[L];
+  load_series<L>(row(0), cur);  // P_0
+#pragma unroll 1
+  for (int i = 1; i <= K - 3; ++i) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push P_{i-1}
+    load_series<L>(row(i), g);
+    trunc_mul_inplace<L>(cur, g);  // P_i
+  }
+  // cur = P_{K-3}
+  load_series<L>(row(K - 2), g);
+  load_series<L>(row(K - 1), S);
+  const double qa = coef<D, L>(cur, g);  // [t^D] P_{K-2}             -> member K-1
+  const double qb = coef<D, L>(cur, S);  // [t^D] P_{K-3} g_{K-1}     -> member K-2
+  trunc_mul_inplace<L>(S, g);            // S_{K-2} = g_{K-2} g_{K-1}
+  double F = 0.0;
+  if constexpr (D >= 1) F = coef<D - 1, L>(cur, S);
+  const double wF = w * F;
+  dep_slot<RB>(K - 1, sid[(K - 1) * TILE], fma(w, qa, wF), ra, sk);
+  dep_slot<RB>(K - 2, sid[(K - 2) * TILE], fma(w, qb, wF), ra, sk);
+#pragma unroll 1
+  for (int i = K - 3; i >= 1; --i) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
+    dep_slot<RB>(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF), ra, sk);
+    load_series<L>(row(i), g);
+    if (i > 1) {
+      trunc_mul_inplace<L>(S, g);  // S_i = g_i S_{i+1}
+    } else {
+      dep_slot<RB>(0, sid[0], fma(w, coef<D, L>(g, S), wF), ra, sk);  // [t^D] g_1 S_2
+    }
+  }
+  if (K == 3) dep_slot<RB>(0, sid[0], fma(w, S[D], wF), ra, sk);  // S = S_1
+}
+
+template <int L, int LMAX, int TILE, int NT, int RB>
+__device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid, double w, const double* xg, int gs,
+                                             double* stk, RunAcc<RB>& ra, const Sink& sk) {
+  if constexpr (L <= LMAX) {
+    if (L_rt == L) {
+      edge_big<L, TILE, NT, RB>(K, sid, w, xg, gs, stk, ra, sk);
+      return;
+    }
+    dispatch_big<L + 1, LMAX, TILE, NT, RB>(L_rt, K, sid, w, xg, gs, stk, ra, sk);
   }
 }
 
@@ -321,8 +403,10 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   constexpr int TILE = Cfg::TILE, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX, NCW = Cfg::NCW, EPL = Cfg::EPL;
   constexpr int RMAX = Cfg::RMAX;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ]
+  // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ] | (large-rank path) prefix
+  // stacks [p.stack_doubles][NCW*32] f64, thread-interleaved
   unsigned char* ring = smem_raw;
+  double* stack = reinterpret_cast<double*>(smem_raw + STAGES * Cfg::STAGE_BYTES);
   const Sink sk{p.priv + (size_t)blockIdx.x * p.H, p.ya, p.H};
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -361,7 +445,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
             bulk_prefetch_l2(p.w + bd.w_off + e0, w_bytes);
           }
         }
-        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+        if (it >= STAGES) mbar_wait_sleep(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
         while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const BucketDesc& bd = p.b[b];
         const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
@@ -375,6 +459,9 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     }
   } else {
     // ---------------- consumer warps
+#if STTSV_BIG_LOCAL
+    double lstk[Cfg::BIG ? big_stack_doubles(KMAX) + 1 : 1];  // large-rank prefix stack (local memory)
+#endif
     RunAcc<RMAX> ra;
 #pragma unroll
     for (int i = 0; i < RMAX; ++i) {
@@ -403,10 +490,16 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
         const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
-        if constexpr (N > 0) {
+        if constexpr (!Cfg::BIG) {
           dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, p.xg, ra, sk, lane);
         } else {
-          warp_block_generic<TILE, EPL>(p.N, k, sids, sw, base, p.xa, sk, lane);
+          const int col = warp * 32 + lane;  // EPL = 1
+#if STTSV_BIG_LOCAL
+          dispatch_big<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, sids + col, sw[col], p.xg, p.gs, lstk, ra, sk);
+#else
+          dispatch_big<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, sids + col, sw[col], p.xg, p.gs,
+                                                      stack + (warp * 32 + lane), ra, sk);
+#endif
         }
       }
       __syncwarp();

@@ -59,7 +59,9 @@ struct EdgeKernelEntry {
   int tile;            // edges per tile
   size_t ring_bytes;   // shared memory of the TMA ring
   int rank;            // N of the instantiation (0 = generic)
-  int run_slots;       // slots with a register run accumulator (EdgeCfg::RMAX; 0 = none)
+  int run_slots;       // slots with a register run accumulator (EdgeCfg::RMAX)
+  int big;             // large-rank path (runtime member loop): 1 prefix stack in shared memory, 2 in local memory
+  int consumers;       // consumer threads per CTA
 };
 #define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry_##n();
 STTSV_COMPILED_RANKS(STTSV_DECLARE_ENTRY)
@@ -68,8 +70,10 @@ EdgeKernelEntry edge_entry_0();
 
 // launchers (kernels.cu)
 EdgeKernelEntry edge_entry(int N);
-// dynamic shared memory of the edge kernel with H shared accumulators
-size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int H);
+// dynamic shared memory of the edge kernel for rank N (TMA ring + large-rank prefix stacks)
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N);
+// doubles of prefix stack per consumer thread of the large-rank path (edge_kernel.cuh)
+int edge_big_stack_doubles(int N);
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
                                cudaStream_t s);

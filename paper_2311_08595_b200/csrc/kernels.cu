@@ -112,7 +112,11 @@ EdgeKernelEntry edge_entry(int N) {
   }
 }
 
-size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int /*H*/) { return e.ring_bytes; }
+int edge_big_stack_doubles(int N) { return big_stack_doubles(N); }
+
+size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N) {
+  return e.ring_bytes + (e.big == 1 ? (size_t)e.consumers * big_stack_doubles(N) * sizeof(double) : 0);
+}
 
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm) {
   cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

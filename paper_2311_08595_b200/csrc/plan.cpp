@@ -473,7 +473,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     DeviceGuard g(device);
     cudaError_t e0 = cudaSetDevice(device);
     if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "cudaSetDevice"); }
-    p->smem = edge_kernel_smem_bytes(p->ent, H);
+    p->smem = edge_kernel_smem_bytes(p->ent, N);
     e0 = edge_kernel_config(p->ent, p->smem, &occ);
     if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "edge kernel configuration"); }
     if (occ < 1) { free_plan(p); return fail(STTSV_ERR_CUDA, "edge kernel cannot be resident (smem %zu)", p->smem); }
