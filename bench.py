@@ -276,7 +276,37 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_tf / fp64_peak,
                          "peak_source": fp64_src,
-                         "flops_def": "2 x FMAs of the per-edge DP incl. series generation (SURVEY.md App. A)"}}
+                         "flops_def": "2 x (FMAs of the per-edge DP, SURVEY.md App. A, + k+1 scalings) per edge; "
+                                      "the series table is per active vertex per apply"}}
+
+    # ---------------- secondary: the same product with STTSV_MERGE_DUPLICATES
+    # (identical vertex sets merged at plan time, weights summed; B is linear in
+    # w).  Reported beside the headline, never as it: the headline stores and
+    # processes every input hyperedge.
+    merged = None
+    if not args.no_merge_report:
+        mplan = S.Plan.from_hypergraph(hg, device=local, world=world, rank=rank, comm=comm,
+                                       flags=S.STTSV_MERGE_DUPLICATES)
+        minfo = mplan.info()
+        for _ in range(args.warmup):
+            mplan.apply(x, y, stream)
+        barrier()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for _ in range(args.steps):
+            mplan.apply(x, y, stream)
+        m1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        mms = m0.elapsed_time(m1) / args.steps
+        if world > 1:
+            t = torch.tensor([mms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            mms = t.item()
+        merged = {"value": hg.incidences / (mms * 1e-3), "unit": UNIT, "ms_per_step": mms,
+                  "stored_edges": minfo["stored_edges"] * world, "input_edges": hg.m,
+                  "note": "STTSV_MERGE_DUPLICATES plan (input incidences / time); not the headline"}
+        mplan.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -297,7 +327,7 @@ def run_ours(args):
                           "kernel_grid": info["kernel_grid"], "kernel_block": info["kernel_block"],
                           "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
                           / (ms_step * 1e-3) / 1e9},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "merge_duplicates": merged,
                "gpu_launches": plan.launches() * args.steps, "clocks": sampler.summary()}
         print(json.dumps(out), flush=True)
     plan.close()
@@ -317,6 +347,7 @@ def main():
     ap.add_argument("--config", default="large", choices=sorted(W.CONFIGS))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-merge-report", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: raising --warmup to 3 (timing rule)")

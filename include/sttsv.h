@@ -70,7 +70,8 @@ typedef enum {
 enum {
   STTSV_CANONICALIZE = 1u << 0,     /* sort each edge's ids instead of rejecting unsorted edges;
                                        repeated ids are still an error                             */
-  STTSV_MERGE_DUPLICATES = 1u << 1, /* reserved (NEXT): merge identical vertex sets, summing weights */
+  STTSV_MERGE_DUPLICATES = 1u << 1, /* merge identical vertex sets of a shard, summing their weights
+                                       (B is linear in w); the plan stores fewer edges */
   STTSV_DETERMINISTIC = 1u << 2     /* reserved (NEXT f2): bit-reproducible reduction order          */
 };
 
@@ -98,7 +99,8 @@ enum {
  *            world/rank: sttsv_apply then all-reduces the active part of y
  *            over NCCL so every rank returns the full s.  With world > 1 and
  *            comm == NULL, sttsv_apply returns only this shard's partial sum.
- *  flags     STTSV_CANONICALIZE; the reserved flags return STTSV_ERR_UNSUPPORTED.
+ *  flags     STTSV_CANONICALIZE, STTSV_MERGE_DUPLICATES; STTSV_DETERMINISTIC (reserved)
+ *            returns STTSV_ERR_UNSUPPORTED.
  *
  * The host arrays are copied; the caller may free them on return.  The plan
  * owns all its device memory until sttsv_plan_destroy.  A plan is immutable
@@ -139,14 +141,16 @@ typedef struct {
   int64_t n;               /* vertex count                                               */
   int32_t rank_Nk;         /* tensor order N                                             */
   int32_t world, rank;     /* shard of this plan                                         */
-  int64_t num_edges;       /* edges stored on this shard                                 */
-  int64_t incidences;      /* sum of |e| over this shard's edges                         */
+  int64_t num_edges;       /* input edges of this shard                                  */
+  int64_t incidences;      /* sum of |e| over this shard's input edges                   */
+  int64_t stored_edges;    /* edges the plan stores (< num_edges with MERGE_DUPLICATES)  */
+  int64_t stored_incidences; /* sum of |e| over the stored edges                         */
   int64_t total_edges;     /* edges in the full input                                    */
   int64_t total_incidences;/* sum of |e| over the full input                             */
   int64_t n_active;        /* vertices of degree >= 1 in the full input                  */
-  int64_t edges_per_size[STTSV_MAX_RANK + 1]; /* this shard's edges of each size           */
+  int64_t edges_per_size[STTSV_MAX_RANK + 1]; /* this shard's input edges of each size     */
   int64_t device_bytes;    /* device memory owned by the plan                            */
-  int64_t stream_bytes;    /* bytes of the edge stream one apply reads (ids + weights)   */
+  int64_t stream_bytes;    /* bytes of the edge stream one apply reads (ids + weights, incl. tile padding) */
   double  fma_per_apply;   /* FP64 fused multiply-adds of the per-edge DP per apply      */
   int32_t hot_private;     /* slots 0..T-1 of every edge accumulate in per-lane register runs */
   int32_t hot_shared;      /* H: ids below H accumulate in CTA shared memory            */

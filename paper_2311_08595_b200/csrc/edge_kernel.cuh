@@ -4,9 +4,11 @@
 // id columns + fp64 weights w' = w (N-1)!/|beta(k)| (PAPER.md:342 footnote and
 // Alg. 2's factor), edges sorted lexicographically by their
 // (degree-relabelled, ascending) member ids.  A tile is TILE = 32*NCW*EPL
-// consecutive edges of one bucket.  One persistent CTA per SM takes a
-// CONTIGUOUS, cost-balanced range of tiles [cta_tiles[b], cta_tiles[b+1])
-// (plan.cpp), so consecutive tiles of a CTA are neighbours in the sort order.
+// consecutive edges of one bucket.  One persistent CTA per SM; its producer
+// grabs CHUNKS of p.chunk consecutive tiles from a global atomic counter (dynamic
+// load balance; tiles ordered most expensive bucket first, so the tail is the
+// cheapest work), so consecutive tiles of a CTA are mostly neighbours in the
+// sort order.
 //
 // Warp specialisation.  Per CTA, one producer warp streams tiles into an
 // STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk ->
@@ -70,9 +72,6 @@ __device__ unsigned long long g_wait_cycles[4];
 #ifndef STTSV_NCW_SMALL
 #define STTSV_NCW_SMALL 15
 #endif
-#ifndef STTSV_PF
-#define STTSV_PF 2
-#endif
 // ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
 // path: runtime member loop, prefix stack in shared memory (edge_big below)
 #ifndef STTSV_BIG_MIN
@@ -112,7 +111,6 @@ struct EdgeCfg {
 #define STTSV_MIN_BLOCKS 1
 #endif
   static constexpr int MIN_BLOCKS = BIG ? 1 : STTSV_MIN_BLOCKS;
-  static constexpr int PF = STTSV_PF;                       // L2 prefetch distance (tiles)
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
 };
@@ -410,7 +408,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   const Sink sk{p.priv + (size_t)blockIdx.x * p.H, p.ya, p.H};
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t t_lo = p.cta_tiles[blockIdx.x], t_hi = p.cta_tiles[blockIdx.x + 1];
+  __shared__ int64_t stile[STAGES];  // tile index staged in each slot (-1: no more work)
 
   for (int j = tid; j < p.H; j += Cfg::THREADS) sk.priv[j] = 0.0;
   if (tid == 0) {
@@ -422,35 +420,31 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   }
   __syncthreads();
 
-  // first bucket of this CTA's range (buckets in tile order; the index only moves forward)
-  int b0 = 0;
-  while (b0 + 1 < p.nb && t_lo >= p.b[b0 + 1].tile_begin) ++b0;
-
   if (warp == NCW) {
-    // ---------------- producer warp: TMA bulk copies of tile t into stage it % STAGES,
-    // plus an L2 prefetch of tile t + PF (hides HBM latency beyond the ring's depth)
+    // ---------------- producer warp: grab chunks of tiles, TMA bulk copies of tile t into
+    // stage it % STAGES, publish t in stile[s] (ordered by the mbarrier's release)
     if (lane == 0) {
-      int b = b0, bp = b0;
-      int64_t it = 0;
-      for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
+      int b = 0;
+      int64_t ct = 0, ce = 0;
+      for (int64_t it = 0;; ++it) {
         const int s = (int)(it % STAGES);
-        if constexpr (Cfg::PF > 0) {
-          const int64_t tp = t + Cfg::PF;
-          if (tp < t_hi) {
-            while (bp + 1 < p.nb && tp >= p.b[bp + 1].tile_begin) ++bp;
-            const BucketDesc& bd = p.b[bp];
-            const int64_t e0 = (tp - bd.tile_begin) * TILE;
-            constexpr uint32_t id_bytes = TILE * 4, w_bytes = TILE * 8;
-            for (int i = 0; i < bd.k; ++i) bulk_prefetch_l2(p.ids + bd.ids_off + i * bd.stride + e0, id_bytes);
-            bulk_prefetch_l2(p.w + bd.w_off + e0, w_bytes);
-          }
-        }
         if (it >= STAGES) mbar_wait_sleep(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+        if (ct == ce) {
+          ct = (int64_t)atomicAdd(p.tile_counter, 1ull) * p.chunk;
+          ce = ct + p.chunk < p.num_tiles ? ct + p.chunk : p.num_tiles;
+        }
+        if (ct >= p.num_tiles) {
+          stile[s] = -1;
+          mbar_arrive_expect_tx(&full[s], 0);
+          break;
+        }
+        const int64_t t = ct++;
         while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const BucketDesc& bd = p.b[b];
         const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
         constexpr uint32_t id_bytes = TILE * 4, w_bytes = TILE * 8;
         unsigned char* st = ring + s * Cfg::STAGE_BYTES;
+        stile[s] = t;
         mbar_arrive_expect_tx(&full[s], id_bytes * bd.k + w_bytes);
         for (int i = 0; i < bd.k; ++i)
           bulk_g2s(st + i * TILE * 4, p.ids + bd.ids_off + i * bd.stride + e0, id_bytes, &full[s]);
@@ -468,16 +462,14 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
       ra.rid[i] = 0;  // flushing (0, 0.0) is a no-op deposit
       ra.run[i] = 0.0;
     }
-    int b = b0;
-    int64_t it = 0;
+    int b = 0;
+    bool any = false;
 #if STTSV_WAITPROF
     long long wait_cyc = 0;
     const long long c_start = clock64();
 #endif
-    for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
+    for (int64_t it = 0;; ++it) {
       const int s = (int)(it % STAGES);
-      while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
-      const int k = p.b[b].k;
       const int base = warp * 32 * EPL;
 #if STTSV_WAITPROF
       const long long w0 = clock64();
@@ -486,6 +478,11 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
 #else
       mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
 #endif
+      const int64_t t = stile[s];
+      if (t < 0) break;
+      any = true;
+      while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
+      const int k = p.b[b].k;
       {
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
@@ -513,7 +510,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     }
 #endif
     // flush the run accumulators
-    if (t_hi > t_lo) {
+    if (any) {
 #pragma unroll
       for (int i = 0; i < RMAX; ++i)
         if (ra.run[i] != 0.0) red_add(sk.at(ra.rid[i]), ra.run[i]);

@@ -45,7 +45,8 @@ struct EdgeKernelParams {
   int32_t H;             // ids < H accumulate in the CTA's private slice of priv
   int32_t tile_edges;    // edges per tile
   int64_t num_tiles;
-  const int64_t* cta_tiles;  // [grid+1]: CTA b processes tiles [cta_tiles[b], cta_tiles[b+1])
+  unsigned long long* tile_counter;  // chunk counter of the dynamic tile scheduler (zeroed per launch)
+  int64_t chunk;         // tiles per grab
 };
 
 // Ranks with a fully unrolled edge kernel (one object file each); every other

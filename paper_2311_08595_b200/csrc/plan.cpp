@@ -185,16 +185,18 @@ static long double scale_constant(int N, int k) {
   return f / surjections_ld(N, k);
 }
 
-// FP64 FMAs of dp_edge<k, N-k+1> (SURVEY.md Appendix A closed form) plus the
-// multiplies of series generation; used for the tile order and plan info.
+// FP64 operations (FMA or MUL) of the per-edge DP for an edge of size k
+// (SURVEY.md Appendix A closed form) plus the k scalings w'(q_i + F); the
+// series table is built once per apply per active vertex, not per edge.  Used
+// for the tile cost balance and plan info (roofline flops = 2 x this).
 static double dp_fma(int N, int k) {
   const double D = N - k, L = D + 1;
   double f;
-  if (k == 1) f = D;
+  if (k == 1) f = 0;
   else if (k == 2) f = D;
   else if (k == 3) f = L * (L + 1) / 2 + 4 * L - 1;
   else f = (k - 3) * L * (L + 1) + (k + 1) * L - 1;
-  return f + 2.0 * k * D;
+  return f + k + 1;
 }
 
 // ------------------------------------------------------------------- plans
@@ -205,6 +207,7 @@ struct sttsv_plan_s {
   int world = 1, rank = 0;
   sttsv_comm_t comm = nullptr;
   int64_t total_edges = 0, total_inc = 0, local_edges = 0, local_inc = 0;
+  int64_t stored_edges = 0, stored_inc = 0;  // after STTSV_MERGE_DUPLICATES
   int64_t n_active = 0;
   int64_t edges_per_size[STTSV_MAX_RANK + 1] = {0};
   // device memory
@@ -311,8 +314,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (world < 1 || rank < 0 || rank >= world) return fail(STTSV_ERR_INVALID_ARGUMENT, "bad world/rank");
   if (comm && (comm->world != world || comm->rank != rank || comm->device != device))
     return fail(STTSV_ERR_INVALID_ARGUMENT, "comm world/rank/device differ from the plan's");
-  if (flags & ~(uint32_t)STTSV_CANONICALIZE)
-    return fail(STTSV_ERR_UNSUPPORTED, "flags 0x%x not implemented in this build", flags & ~(uint32_t)STTSV_CANONICALIZE);
+  const uint32_t known = STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES;
+  if (flags & ~known) return fail(STTSV_ERR_UNSUPPORTED, "flags 0x%x not implemented in this build", flags & ~known);
 
   // ---- validate; offsets
   std::vector<int64_t> off(m + 1, 0);
@@ -413,6 +416,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     rows_total += (int64_t)k * mk[k];
   }
   std::vector<int32_t> rows((size_t)rows_total);
+  std::vector<int64_t> stored(N + 1, 0);  // edges stored per bucket (after optional merging)
   std::vector<double> wrow((size_t)w_total);
 #pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < m; ++e) {
@@ -447,17 +451,36 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     });
     int32_t* col = h_ids.data() + ids_off[k];
     const int64_t st = stride[k];
+    int64_t kept = mk[k];
+    if (flags & STTSV_MERGE_DUPLICATES) {
+      // identical vertex sets are adjacent after the sort: keep the first of each
+      // run with the run's summed weight (B is linear in w)
+      kept = 0;
+      for (int64_t j = 0; j < mk[k];) {
+        const int32_t* src = R + perm[j] * k;
+        long double wsum = 0.0L;
+        int64_t j2 = j;
+        while (j2 < mk[k] && std::equal(src, src + k, R + perm[j2] * k)) wsum += (long double)wrow[w_off[k] + perm[j2++]];
+        for (int i = 0; i < k; ++i) col[(int64_t)i * st + kept] = src[i];
+        h_w[w_off[k] + kept] = (double)wsum;
+        ++kept;
+        j = j2;
+      }
+    } else {
 #pragma omp parallel for schedule(static)
-    for (int64_t j = 0; j < mk[k]; ++j) {
-      const int32_t* src = R + perm[j] * k;
-      for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = src[i];
-      h_w[w_off[k] + j] = wrow[w_off[k] + perm[j]];
+      for (int64_t j = 0; j < mk[k]; ++j) {
+        const int32_t* src = R + perm[j] * k;
+        for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = src[i];
+        h_w[w_off[k] + j] = wrow[w_off[k] + perm[j]];
+      }
     }
+    stored[k] = kept;
     // pad the bucket to whole tiles with copies of its last edge at weight 0:
     // the kernel then never meets a partial tile (no per-lane validity tests),
     // a padded edge contributes exactly 0 and continues the last edge's runs
-    for (int64_t j = mk[k]; j < st; ++j) {
-      for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = col[(int64_t)i * st + mk[k] - 1];
+    const int64_t padded = (kept + tile - 1) / tile * tile;
+    for (int64_t j = kept; j < padded; ++j) {
+      for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = col[(int64_t)i * st + kept - 1];
       h_w[w_off[k] + j] = 0.0;
     }
   }
@@ -491,13 +514,16 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     const int k = order[i];
     BucketDesc& b = kp.b[i];
     b.k = k;
-    b.m = mk[k];
+    b.m = stored[k];
     b.stride = stride[k];
     b.tile_begin = tiles;
     b.ids_off = ids_off[k];
     b.w_off = w_off[k];
-    tiles += stride[k] / tile;
-    fma += dp_fma(N, k) * (double)mk[k];
+    tiles += (stored[k] + tile - 1) / tile;
+    fma += dp_fma(N, k) * (double)stored[k];
+    p->stored_edges += stored[k];
+    p->stored_inc += stored[k] * k;
+    p->stream_bytes += (stored[k] + tile - 1) / tile * tile * (4 * k + 8);
   }
   kp.num_tiles = tiles;
   kp.n_active = (int32_t)na;
@@ -505,40 +531,17 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.H = H;
   kp.tile_edges = tile;
   p->fma = fma;
-  p->stream_bytes = ids_total * 4 + w_total * 8;
 
-  // ---- persistent grid: one contiguous range of tiles per CTA, balanced by an
-  // estimated per-edge cost (stream bytes + FP64 work + per-incidence scatter)
+  // ---- persistent grid: one CTA per SM (x occupancy); tiles are grabbed in chunks
+  // from a device counter (edge_kernel.cuh), which balances the load dynamically
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int64_t grid = (int64_t)sms * std::max(occ, 1);
   if (grid > tiles) grid = std::max<int64_t>(tiles, 1);
-  std::vector<int64_t> cta_tiles(grid + 1, tiles);
-  {
-    std::vector<double> tcost(tiles + 1, 0.0);  // prefix cost over tiles
-    int64_t t = 0;
-    for (int i = 0; i < kp.nb; ++i) {
-      const int k = kp.b[i].k;
-      const double per_edge = (4.0 * k + 8.0) + 0.5 * dp_fma(N, k) + 6.0 * k;
-      const int64_t nt = (kp.b[i].m + tile - 1) / tile;
-      for (int64_t j = 0; j < nt; ++j, ++t) {
-        const int64_t cnt = std::min<int64_t>(tile, kp.b[i].m - j * tile);
-        tcost[t + 1] = tcost[t] + per_edge * (double)cnt;
-      }
-    }
-    const double total = tcost[tiles];
-    int64_t c = 0;
-    cta_tiles[0] = 0;
-    for (int64_t b = 1; b < grid; ++b) {
-      const double target = total * (double)b / (double)grid;
-      while (c < tiles && tcost[c + 1] <= target) ++c;
-      // round to the nearer boundary
-      int64_t cut = c;
-      if (c < tiles && target - tcost[c] > tcost[c + 1] - target) cut = c + 1;
-      cta_tiles[b] = std::max(cut, cta_tiles[b - 1]);
-    }
-    cta_tiles[grid] = tiles;
-  }
+  // chunk: long enough for run continuity, short enough that the tail (the
+  // cheapest bucket) balances: about 1/16 of a CTA's fair share
+  kp.chunk = std::max<int64_t>(1, tiles / (grid * 16));
+  if (const char* env = getenv("STTSV_CHUNK")) kp.chunk = std::max(1, atoi(env));
 
   // ---- device memory: one allocation
   DeviceGuard g(device);
@@ -547,7 +550,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
                b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8);
   const int gs = series_stride(N);
   const size_t b_xg = align((size_t)na * gs * 8 + 16);
-  const size_t b_cta = align((size_t)(grid + 1) * 8);
+  const size_t b_cta = align(8);
   const size_t b_priv = align((size_t)grid * H * 8 + 8);
   p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
@@ -560,13 +563,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->d_ya = (double*)(base + b_ids + b_w + b_act + b_xa);
   p->d_scratch = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya);
   p->d_xg = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
-  int64_t* d_cta = (int64_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg);
+  unsigned long long* d_cnt = (unsigned long long*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg);
   double* d_priv = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta);
   p->gs = gs;
   if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess) ce = cudaMemcpy(d_cta, cta_tiles.data(), (grid + 1) * 8, cudaMemcpyHostToDevice);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
   kp.ids = d_ids;
   kp.w = d_w;
@@ -574,7 +576,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.xg = p->d_xg;
   kp.gs = gs;
   kp.ya = p->d_ya;
-  kp.cta_tiles = d_cta;
+  kp.tile_counter = d_cnt;
   kp.priv = d_priv;
 
   p->grid = (int)grid;
@@ -592,6 +594,8 @@ extern "C" sttsv_status_t sttsv_plan_info(sttsv_plan_t p, sttsv_plan_info_t* inf
   info->rank = p->rank;
   info->num_edges = p->local_edges;
   info->incidences = p->local_inc;
+  info->stored_edges = p->stored_edges;
+  info->stored_incidences = p->stored_inc;
   info->total_edges = p->total_edges;
   info->total_incidences = p->total_inc;
   info->n_active = p->n_active;
@@ -664,6 +668,7 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
       ev = &p->events[p->events_used++];
       CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
     }
+    CUDA_TRY(cudaMemsetAsync(p->kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
     CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s), "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }

@@ -37,6 +37,7 @@ class SttsvError(RuntimeError):
 class PlanInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("rank_Nk", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("num_edges", ctypes.c_int64), ("incidences", ctypes.c_int64),
+                ("stored_edges", ctypes.c_int64), ("stored_incidences", ctypes.c_int64),
                 ("total_edges", ctypes.c_int64), ("total_incidences", ctypes.c_int64),
                 ("n_active", ctypes.c_int64), ("edges_per_size", ctypes.c_int64 * (MAX_RANK + 1)),
                 ("device_bytes", ctypes.c_int64), ("stream_bytes", ctypes.c_int64),

@@ -247,3 +247,17 @@ def test_full_size_sampled(S, torch_cuda, name):
     del plan
     y1, plan = gpu_apply(S, torch, hg, x=np.ones(hg.n), weights=None)
     assert rel(y1, deg.astype(np.float64)) < TOL
+
+
+@pytest.mark.parametrize("name,m", [("mid", 300_000), ("large", 400_000), ("high-rank", 2_000)])
+def test_merge_duplicates(S, torch_cuda, name, m):
+    """STTSV_MERGE_DUPLICATES: identical vertex sets merged with summed weights
+    (B is linear in w) — same product, fewer stored edges."""
+    hg = W.generate(name, m=m)
+    y, plan = gpu_apply(S, torch_cuda, hg, flags=S.STTSV_MERGE_DUPLICATES)
+    info = plan.info()
+    assert info["num_edges"] == hg.m and info["stored_edges"] < hg.m
+    # distinct vertex sets counted independently of the library
+    keys = {hg.edge(e).tobytes() for e in range(hg.m)}
+    assert info["stored_edges"] == len(keys)
+    assert rel(y, oracle.sttsv(hg)) < TOL
