@@ -136,6 +136,22 @@ sttsv_status_t sttsv_apply_host(sttsv_plan_t plan, const double* x_host, double*
  * allreduce of the active part of z.  Requires N >= 2 and iters >= 0. */
 sttsv_status_t sttsv_power_iterate(sttsv_plan_t plan, double* x_dev, double* z_dev, int iters, void* stream);
 
+/* sttsv_hec — H-eigenvector centrality by the NQZ iteration, Alg. 1 of the
+ * paper, with the lambda bracket of lines 8-9:
+ *   y = x_dev (on entry: x_0, e.g. (1/n) 1, line 3);  z = B y^{N-1} (line 4);
+ *   repeat:  x = z^[1/(N-1)] / ||z^[1/(N-1)]||_1   (line 6)
+ *            z = B x^{N-1}                          (line 7)
+ *            lambda_min = min(z ./ x^[N-1]),  lambda_max = max(z ./ x^[N-1])   (lines 8-9)
+ *   until (lambda_max - lambda_min) / lambda_min < tau  or  max_iters repetitions.
+ * Min/max run over vertices with x_v > 0 (reading A15 of DESIGN.md: isolated
+ * vertices have x_v = 0).  On return x_dev (device fp64[n]) holds x, z_dev
+ * (device fp64[n] or NULL) the last z, *lambda_min / *lambda_max the last
+ * bracket and *iters_done the repetitions run.  Synchronous: the host reads the
+ * bracket after every repetition.  tau >= 0 (0 runs exactly max_iters);
+ * max_iters >= 1; N >= 2.  With a comm each STTSV costs one allreduce. */
+sttsv_status_t sttsv_hec(sttsv_plan_t plan, double* x_dev, double* z_dev, double tau, int max_iters,
+                         double* lambda_min, double* lambda_max, int* iters_done, void* stream);
+
 /* Plan introspection (host values; no device work). */
 typedef struct {
   int64_t n;               /* vertex count                                               */

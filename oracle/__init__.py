@@ -144,3 +144,32 @@ def power_iteration(hg, iters: int, rank=None, x0=None, nthreads: int = 0):
         r = np.power(z, 1.0 / (N - 1))
         x = r / r.sum()
     return x, z
+
+
+def nqz(hg, tau: float, max_iters: int, rank=None, x0=None, nthreads: int = 0, history: bool = False):
+    """Alg. 1 (NQZ, H-eigenvector centrality), line by line:
+    y = (1/n) 1 (line 3); z = TTSV1(y) (line 4); repeat { x = z^[1/(N-1)] / ||z^[1/(N-1)]||_1 (line 6);
+    z = TTSV1(x) (line 7); lambda_min = min(z ./ x^[N-1]) (line 8); lambda_max = max(...) (line 9) }
+    until (lambda_max - lambda_min)/lambda_min < tau (line 10) or max_iters repetitions.
+    min/max over x_v > 0 (reading A15 of DESIGN.md).  Returns (x, z, lambda_min, lambda_max, iters)
+    and, with history=True, also the list of (lambda_min, lambda_max) per repetition."""
+    N = hg.rank if rank is None else int(rank)
+    y = np.full(hg.n, 1.0 / hg.n) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
+    z = sttsv(hg, x=y, rank=N, nthreads=nthreads)
+    hist = []
+    it = 0
+    x = y
+    lo = hi = 0.0
+    while it < max_iters:
+        r = np.power(z, 1.0 / (N - 1))
+        x = r / r.sum()
+        z = sttsv(hg, x=x, rank=N, nthreads=nthreads)
+        pos = x > 0
+        ratio = z[pos] / np.power(x[pos], N - 1)
+        lo, hi = float(ratio.min()), float(ratio.max())
+        hist.append((lo, hi))
+        it += 1
+        if (hi - lo) / lo < tau:
+            break
+    out = (x, z, lo, hi, it)
+    return out + (hist,) if history else out

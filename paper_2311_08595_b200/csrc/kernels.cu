@@ -99,6 +99,68 @@ __global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __r
   }
 }
 
+// Alg. 1 lines 8-9: lambda_min/max of z ./ x^[N-1] over x > 0
+// (reading A15: isolated vertices, x = 0, are excluded).  Per-block partials,
+// then one block combines them.
+__global__ void __launch_bounds__(kNormBlock) lambda_partial_kernel(const double* __restrict__ z,
+                                                                   const double* __restrict__ x,
+                                                                   double* __restrict__ partial, int64_t n,
+                                                                   int Nm1) {
+  __shared__ double smin[32], smax[32];
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double xv = x[i];
+    if (xv > 0.0) {
+      double p = 1.0;
+      for (int j = 0; j < Nm1; ++j) p *= xv;
+      const double r = z[i] / p;
+      lo = fmin(lo, r);
+      hi = fmax(hi, r);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    smin[warp] = lo;
+    smax[warp] = hi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    lo = lane < (int)(blockDim.x >> 5) ? smin[lane] : INFINITY;
+    hi = lane < (int)(blockDim.x >> 5) ? smax[lane] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      partial[2 * blockIdx.x] = lo;
+      partial[2 * blockIdx.x + 1] = hi;
+    }
+  }
+}
+
+__global__ void lambda_final_kernel(const double* __restrict__ partial, int nparts, double* __restrict__ out) {
+  double lo = INFINITY, hi = -INFINITY;
+  for (int j = threadIdx.x; j < nparts; j += 32) {
+    lo = fmin(lo, partial[2 * j]);
+    hi = fmax(hi, partial[2 * j + 1]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (threadIdx.x == 0) {
+    out[0] = lo;
+    out[1] = hi;
+  }
+}
+
 // ------------------------------------------------------------- launchers
 EdgeKernelEntry edge_entry(int N) {
   switch (N) {
@@ -147,6 +209,15 @@ cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, doubl
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
   expand_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(ya, act, y, n_active);
+  return cudaGetLastError();
+}
+
+// out[0..1] = (lambda_min, lambda_max); `partial` holds 2 * kNormalizeScratch doubles
+cudaError_t launch_lambda(const double* z, const double* x, double* partial, double* out, int64_t n_active, int N,
+                          cudaStream_t s) {
+  const int grid = grid_for(n_active, kNormBlock, kNormMaxGrid);
+  lambda_partial_kernel<<<grid, kNormBlock, 0, s>>>(z, x, partial, n_active, N - 1);
+  lambda_final_kernel<<<1, 32, 0, s>>>(partial, grid, out);
   return cudaGetLastError();
 }
 

@@ -223,6 +223,7 @@ struct sttsv_plan_s {
   double* d_xhost = nullptr;
   double* d_yhost = nullptr;
   cudaStream_t host_stream = nullptr;
+  double* h_lambda = nullptr;  // pinned (lambda_min, lambda_max) of sttsv_hec
   // kernel
   EdgeKernelEntry ent{};
   EdgeKernelParams kp{};
@@ -293,6 +294,7 @@ static void free_plan(sttsv_plan_s* p) {
   if (p->dmem) cudaFree(p->dmem);
   if (p->d_xhost) cudaFree(p->d_xhost);
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
+  if (p->h_lambda) cudaFreeHost(p->h_lambda);
   delete p;
 }
 
@@ -547,7 +549,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   DeviceGuard g(device);
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t b_ids = align(ids_total * 4), b_w = align(w_total * 8), b_act = align(na * 4 + 4),
-               b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align(kNormalizeScratch * 8);
+               b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align((2 * kNormalizeScratch + 4) * 8);
   const int gs = series_stride(N);
   const size_t b_xg = align((size_t)na * gs * 8 + 16);
   const size_t b_cta = align(8);
@@ -744,5 +746,52 @@ extern "C" sttsv_status_t sttsv_power_iterate(sttsv_plan_t p, double* x, double*
     CUDA_TRY(cudaMemsetAsync(z, 0, bytes, s), "memset z");
     CUDA_TRY(launch_expand(p->d_ya, p->d_act, z, p->n_active, s), "expand z");
   }
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_hec(sttsv_plan_t p, double* x, double* z, double tau, int max_iters,
+                                    double* lambda_min, double* lambda_max, int* iters_done, void* stream) {
+  if (!p || !x || !lambda_min || !lambda_max || !iters_done) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (max_iters < 1) return fail(STTSV_ERR_INVALID_ARGUMENT, "max_iters < 1");
+  if (!(tau >= 0.0)) return fail(STTSV_ERR_INVALID_ARGUMENT, "tau must be >= 0");
+  if (p->N < 2) return fail(STTSV_ERR_INVALID_ARGUMENT, "HEC needs rank >= 2");
+  const size_t bytes = (size_t)p->n * sizeof(double);
+  if (z && overlap(x, bytes, z, bytes)) return fail(STTSV_ERR_ALIAS, "x and z overlap");
+  DeviceGuard g(p->device);
+  sttsv_status_t st = check_async(p);
+  if (st != STTSV_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p->h_lambda) CUDA_TRY(cudaMallocHost(&p->h_lambda, 2 * sizeof(double)), "cudaMallocHost");
+  double* d_lam = p->d_scratch + 2 * kNormalizeScratch;
+  // Alg. 1: y = x0 (caller's, e.g. (1/n) 1); z = TTSV1(y)
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->n_active, s), "gather launch");
+  st = apply_active(p, s);
+  if (st != STTSV_OK) return st;
+  double lo = 0.0, hi = 0.0;
+  int it = 0;
+  while (it < max_iters) {
+    // x = z^[1/(N-1)] / ||z^[1/(N-1)]||_1 ; z = TTSV1(x) ; lambda bracket of z ./ x^[N-1]
+    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_xg, p->gs, p->d_scratch, p->n_active, p->N, s),
+             "normalize launch");
+    st = apply_active(p, s);
+    if (st != STTSV_OK) return st;
+    CUDA_TRY(launch_lambda(p->d_ya, p->d_xa, p->d_scratch, d_lam, p->n_active, p->N, s), "lambda launch");
+    CUDA_TRY(cudaMemcpyAsync(p->h_lambda, d_lam, 2 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
+    CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+    ++it;
+    lo = p->h_lambda[0];
+    hi = p->h_lambda[1];
+    if ((hi - lo) / lo < tau) break;  // until (lambda_max - lambda_min) / lambda_min < tau
+  }
+  CUDA_TRY(cudaMemsetAsync(x, 0, bytes, s), "memset x");
+  CUDA_TRY(launch_expand(p->d_xa, p->d_act, x, p->n_active, s), "expand x");
+  if (z) {
+    CUDA_TRY(cudaMemsetAsync(z, 0, bytes, s), "memset z");
+    CUDA_TRY(launch_expand(p->d_ya, p->d_act, z, p->n_active, s), "expand z");
+  }
+  CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+  *lambda_min = lo;
+  *lambda_max = hi;
+  *iters_done = it;
   return STTSV_OK;
 }

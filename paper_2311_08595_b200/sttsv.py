@@ -71,6 +71,8 @@ def load():
         "sttsv_apply": ([P, P, P, P], st),
         "sttsv_apply_host": ([P, P, P], st),
         "sttsv_power_iterate": ([P, P, P, ctypes.c_int, P], st),
+        "sttsv_hec": ([P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), P], st),
         "sttsv_plan_info": ([P, ctypes.POINTER(PlanInfo)], st),
         "sttsv_apply_launches": ([P], ctypes.c_int),
         "sttsv_plan_profile": ([P, ctypes.c_int], st),
@@ -93,6 +95,7 @@ def load():
 
 def exported_symbols() -> list[str]:
     return ["sttsv_plan_create", "sttsv_plan_destroy", "sttsv_apply", "sttsv_apply_host", "sttsv_power_iterate",
+            "sttsv_hec",
             "sttsv_plan_info", "sttsv_apply_launches", "sttsv_plan_profile", "sttsv_plan_profile_read",
             "sttsv_shard_edges", "sttsv_comm_unique_id",
             "sttsv_comm_create", "sttsv_comm_destroy", "sttsv_status_string", "sttsv_last_error", "sttsv_version"]
@@ -146,6 +149,14 @@ def sttsv_apply_host(plan, x_host: np.ndarray, y_host: np.ndarray):
 
 def sttsv_power_iterate(plan, x_dev, z_dev, iters, stream=None):
     _check(load().sttsv_power_iterate(plan, _ptr(x_dev), _ptr(z_dev), int(iters), _stream_ptr(stream, x_dev.device)))
+
+
+def sttsv_hec(plan, x_dev, z_dev, tau, max_iters, stream=None):
+    """Alg. 1 (NQZ) with the lambda bracket; returns (lambda_min, lambda_max, iters_done)."""
+    lo, hi, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    _check(load().sttsv_hec(plan, _ptr(x_dev), _ptr(z_dev), float(tau), int(max_iters), ctypes.byref(lo),
+                            ctypes.byref(hi), ctypes.byref(it), _stream_ptr(stream, x_dev.device)))
+    return lo.value, hi.value, it.value
 
 
 def sttsv_plan_info(plan) -> dict:
@@ -265,6 +276,16 @@ class Plan:
         self._check_vec(z)
         sttsv_power_iterate(self._h, x, z, iters, stream)
         return x, z
+
+    def hec(self, x, tau, max_iters, z=None, stream=None):
+        """H-eigenvector centrality (Alg. 1): x in = x_0, out = x; returns (x, z, lmin, lmax, iters)."""
+        import torch
+        self._check_vec(x)
+        if z is None:
+            z = torch.empty_like(x)
+        self._check_vec(z)
+        lo, hi, it = sttsv_hec(self._h, x, z, tau, max_iters, stream)
+        return x, z, lo, hi, it
 
     def _check_vec(self, t):
         import torch

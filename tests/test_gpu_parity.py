@@ -261,3 +261,28 @@ def test_merge_duplicates(S, torch_cuda, name, m):
     keys = {hg.edge(e).tobytes() for e in range(hg.m)}
     assert info["stored_edges"] == len(keys)
     assert rel(y, oracle.sttsv(hg)) < TOL
+
+
+def test_hec_matches_oracle(S, torch_cuda):
+    """sttsv_hec (Alg. 1 with the lambda bracket) against oracle.nqz: a fixed number of
+    repetitions (tau = 0) must agree to the parity bound; a converged run must stop with a
+    bracket below tau within a couple of repetitions of the oracle (where the stopping test
+    lands is decided by the last bits of lambda, so the counts may differ by one or two)."""
+    torch = torch_cuda
+    hg = W.generate("centrality", m=40_000, n=200_000)
+    plan = S.Plan.from_hypergraph(hg)
+    x0 = torch.full((hg.n,), 1.0 / hg.n, dtype=torch.float64, device="cuda")
+    xo, zo, lo_o, hi_o, it_o = oracle.nqz(hg, tau=0.0, max_iters=25)
+    x, z, lo, hi, it = plan.hec(x0.clone(), 0.0, 25)
+    torch.cuda.synchronize()
+    assert it == it_o == 25
+    assert rel(x.cpu().numpy(), xo) < TOL and rel(z.cpu().numpy(), zo) < TOL
+    assert abs(lo - lo_o) <= TOL * abs(lo_o) and abs(hi - hi_o) <= TOL * abs(hi_o)
+    tau = 1e-9
+    xo, zo, lo_o, hi_o, it_o = oracle.nqz(hg, tau=tau, max_iters=400)
+    x, z, lo, hi, it = plan.hec(x0.clone(), tau, 400)
+    torch.cuda.synchronize()
+    assert (hi - lo) / lo < tau and (hi_o - lo_o) / lo_o < tau
+    assert abs(it - it_o) <= 3, (it, it_o)
+    assert rel(x.cpu().numpy(), xo) < 1e-8    # both within the converged bracket
+    plan.close()

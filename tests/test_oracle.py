@@ -278,3 +278,36 @@ def test_power_iteration_pins():
     assert rel_err(x3, x1) < 1e-14 and rel_err(z3, 3 * z1) < 1e-14
     deg = np.bincount(hg.indices, minlength=hg.n)
     assert np.all(x1[deg == 0] == 0) and abs(x1.sum() - 1) < 1e-14
+
+
+# ------------------------------------------------------------- NQZ / HEC (f1) ----
+def test_nqz_pins():
+    """Alg. 1 with the lambda bracket (PAPER.md:346-364)."""
+    # single edge {0,1}, N = 2, w = 2: x = (1/2, 1/2), lambda = 1 (SPEC.md:453)
+    x, z, lo, hi, it = oracle.nqz(to_hg(2, 2, [[0, 1]], [2.0], [0, 0]), tau=1e-12, max_iters=10)
+    assert it == 1 and np.allclose(x, 0.5, rtol=0, atol=1e-15)
+    assert abs(lo - 1.0) < 1e-15 and abs(hi - 1.0) < 1e-15
+    # vertex-transitive 3-uniform (all 3-subsets of 6), w = 3: uniform x and, for a uniform
+    # hypergraph (k = N), z_v = (w/N) sum_{e ∋ v} prod_{u != v} x_u  =>  lambda = deg(v) w / N = 10
+    edges = [list(c) for c in itertools.combinations(range(6), 3)]
+    x, z, lo, hi, it = oracle.nqz(to_hg(6, 3, edges, [3.0] * len(edges), np.zeros(6)), tau=1e-13, max_iters=20)
+    assert np.allclose(x, 1 / 6, rtol=0, atol=1e-15)
+    assert abs(lo - 10.0) < 1e-12 and abs(hi - 10.0) < 1e-12
+
+
+def test_nqz_bracket_monotone_and_eigen_residual():
+    """Collatz-Wielandt / NQZ: for a connected hypergraph the bracket [lambda_min, lambda_max]
+    shrinks monotonically and brackets the H-eigenvalue; at convergence B x^{N-1} = lambda x^[N-1]."""
+    rng = np.random.default_rng(4)
+    n, N = 12, 4
+    edges = [sorted(rng.choice(n, size=int(rng.integers(2, N + 1)), replace=False).tolist()) for _ in range(40)]
+    edges += [[i, i + 1] for i in range(n - 1)]        # a path makes it connected
+    hg = to_hg(n, N, edges, rng.uniform(0.5, 2.0, len(edges)), np.zeros(n))
+    x, z, lo, hi, it, hist = oracle.nqz(hg, tau=1e-13, max_iters=500, history=True)
+    los = [a for a, _ in hist]
+    his = [b for _, b in hist]
+    assert all(b >= a - 1e-12 * abs(a) for a, b in zip(los[:-1], los[1:]))     # lambda_min non-decreasing
+    assert all(b <= a + 1e-12 * abs(a) for a, b in zip(his[:-1], his[1:]))     # lambda_max non-increasing
+    assert (hi - lo) / lo < 1e-13 and it < 500
+    lam = 0.5 * (lo + hi)
+    assert rel_err(oracle.sttsv(hg, x=x), lam * x ** (N - 1)) < 1e-12
