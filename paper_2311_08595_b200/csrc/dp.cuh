@@ -79,16 +79,10 @@ __device__ __forceinline__ double coef(const double (&a)[L], const double (&b)[L
   return s;
 }
 
-// K >= 2 members with series g[i][0..L-1].  P[i] = g_0 * ... * g_i (i = 0..K-3)
-// are the prefix products; the caller keeps P between consecutive edges and
-// passes h = the number of leading members this edge shares with the previous
-// one (warp-uniform): P[i] depends on members 0..i only, so P[0..h-1] are
-// reused and only P[h..K-3] are recomputed (memoised shared prefixes — the idea
-// of the paper's CCSS-MEMO, Alg. 4, applied along the sorted
-// edge order).  h = 0 recomputes everything.
-template <int K, int L, int KP = (K > 2 ? K - 2 : 1)>
-__device__ __forceinline__ void dp_core(const double (&g)[K][L], double (&P)[KP][L], int h, double (&q)[K],
-                                        double& F) {
+// K >= 2 members with series g[i][0..L-1]; prefix products P[i] = g_0 * ... * g_i
+// (i = 0..K-3) and a running suffix S.
+template <int K, int L>
+__device__ __forceinline__ void dp_core(const double (&g)[K][L], double (&q)[K], double& F) {
   static_assert(K >= 2, "dp_core needs K >= 2");
   constexpr int D = L - 1;
   F = 0.0;
@@ -97,13 +91,11 @@ __device__ __forceinline__ void dp_core(const double (&g)[K][L], double (&P)[KP]
     q[0] = g[1][D];
     q[1] = g[0][D];
   } else {
-    if (h < 1) {
+    double P[K - 2][L];
 #pragma unroll
-      for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
-    }
+    for (int j = 0; j < L; ++j) P[0][j] = g[0][j];
 #pragma unroll
-    for (int i = 1; i <= K - 3; ++i)
-      if (i >= h) trunc_mul<L>(P[i - 1], g[i], P[i]);
+    for (int i = 1; i <= K - 3; ++i) trunc_mul<L>(P[i - 1], g[i], P[i]);
     // last two members
     q[K - 1] = coef<D, L>(P[K - 3], g[K - 2]);   // [t^D] P_{K-2}
     q[K - 2] = coef<D, L>(P[K - 3], g[K - 1]);   // [t^D] P_{K-3} S_{K-1}
@@ -126,90 +118,19 @@ __device__ __forceinline__ void dp_core(const double (&g)[K][L], double (&P)[KP]
   }
 }
 
-// One edge from the series table: rows[i] = table row of member i; P / h as in
-// dp_core (g_0 enters only through P[0], so its row is not loaded when h >= 1).
-template <int K, int L, int KP = (K > 2 ? K - 2 : 1)>
-__device__ __forceinline__ void dp_edge_table(const double* const (&rows)[K], double (&P)[KP][L], int h,
-                                              double (&q)[K], double& F) {
+// One edge from the series table: rows[i] = table row of member i.
+template <int K, int L>
+__device__ __forceinline__ void dp_edge_table(const double* const (&rows)[K], double (&q)[K], double& F) {
   constexpr int D = L - 1;
   if constexpr (K == 1) {
     // singleton: Q = 1 (empty product), F = g_0:  q = [D == 0],  F[D-1] = x^D / D!
     q[0] = D == 0 ? 1.0 : 0.0;
-    F = D >= 1 ? __ldg(rows[0] + (D - 1)) : 0.0;
+    F = D >= 1 ? __ldg(rows[0] + (D >= 1 ? D - 1 : 0)) : 0.0;
   } else {
     double g[K][L];
-    if (K == 2 || h < 1) load_series<L>(rows[0], g[0]);
 #pragma unroll
-    for (int i = 1; i < K; ++i) load_series<L>(rows[i], g[i]);
-    dp_core<K, L>(g, P, h, q, F);
-  }
-}
-
-// reload of a table row that the compiler must not merge with an earlier load
-// of the same row (keeps the row out of registers between the two uses)
-template <int L>
-__device__ __forceinline__ void reload_series(const double* __restrict__ row, double (&g)[L]) {
-#pragma unroll
-  for (int j = 0; j < L; j += 2) {
-    double a, b;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(row + j));
-    g[j] = a;
-    if (j + 1 < L) g[j + 1] = b;
-  }
-}
-
-// The same DP with a small register footprint: each g row is loaded when it is
-// used (prefix pass g_0..g_{K-3}, then g_{K-2}, g_{K-1}) and g_{K-3}..g_1 are
-// re-read from the (L1-resident) table in the suffix pass instead of being held.
-// Live state: the prefix products P (K-2 rows), two rows and the suffix S.
-template <int K, int L>
-__device__ __forceinline__ void dp_edge_lean(const double* const (&rows)[K], double (&q)[K], double& F) {
-  constexpr int D = L - 1;
-  F = 0.0;
-  if constexpr (K == 1) {
-    q[0] = D == 0 ? 1.0 : 0.0;
-    F = D >= 1 ? __ldg(rows[0] + (D - 1)) : 0.0;
-  } else if constexpr (K == 2) {
-    double a[L], b[L];
-    load_series<L>(rows[0], a);
-    load_series<L>(rows[1], b);
-    if constexpr (D >= 1) F = coef<D - 1, L>(a, b);
-    q[0] = b[D];
-    q[1] = a[D];
-  } else {
-    double P[K - 2][L];
-    load_series<L>(rows[0], P[0]);
-#pragma unroll
-    for (int i = 1; i <= K - 3; ++i) {
-      double gi[L];
-      load_series<L>(rows[i], gi);
-      trunc_mul<L>(P[i - 1], gi, P[i]);
-    }
-    double S[L];
-    {
-      double ga[L], gb[L];
-      load_series<L>(rows[K - 2], ga);
-      load_series<L>(rows[K - 1], gb);
-      q[K - 1] = coef<D, L>(P[K - 3], ga);       // [t^D] P_{K-2}
-      q[K - 2] = coef<D, L>(P[K - 3], gb);       // [t^D] P_{K-3} S_{K-1}
-      trunc_mul<L>(ga, gb, S);                    // S_{K-2}
-    }
-    if constexpr (D >= 1) F = coef<D - 1, L>(P[K - 3], S);   // [t^{D-1}] P_{K-3} S_{K-2}
-#pragma unroll
-    for (int i = K - 3; i >= 1; --i) {
-      q[i] = coef<D, L>(P[i - 1], S);            // [t^D] P_{i-1} S_{i+1}
-      double gi[L];
-      reload_series<L>(rows[i], gi);
-      if (i > 1) {
-        double T[L];
-        trunc_mul<L>(gi, S, T);                   // S_i
-#pragma unroll
-        for (int j = 0; j < L; ++j) S[j] = T[j];
-      } else {
-        q[0] = coef<D, L>(gi, S);                 // [t^D] g_1 S_2
-      }
-    }
-    if constexpr (K == 3) q[0] = S[D];           // S = S_1
+    for (int i = 0; i < K; ++i) load_series<L>(rows[i], g[i]);
+    dp_core<K, L>(g, q, F);
   }
 }
 

@@ -53,15 +53,6 @@ constexpr unsigned kFull = 0xffffffffu;
 __device__ unsigned long long g_wait_cycles[4];
 #endif
 
-// Prefix memoisation along a lane's consecutive edges (dp.cuh dp_core, h > 0);
-// compile-time switch for A/B timing (0 = recompute every prefix).
-#ifndef STTSV_MEMO
-#define STTSV_MEMO 0
-#endif
-// Register-lean DP (dp.cuh dp_edge_lean): rows re-read in the suffix pass.
-#ifndef STTSV_LEAN
-#define STTSV_LEAN 0
-#endif
 
 #ifndef STTSV_EPL
 #define STTSV_EPL 5
@@ -225,12 +216,11 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
                                            const double* __restrict__ xg, RunAcc<RMAX>& ra, const Sink& sk,
                                            int lane) {
   constexpr int L = N - K + 1;
-  constexpr int KP = K > 2 ? K - 2 : 1;
   constexpr int GS = series_stride(N);
-  double P[KP][L];  // prefix products, kept between this lane's consecutive edges
+  const int col0 = base + lane * EPL;
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
-    const int col = base + lane * EPL + r;
+    const int col = col0 + r;
     int id[K];
     const double* rows[K];
 #pragma unroll
@@ -238,25 +228,9 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
       id[i] = sids[i * TILE + col];
       rows[i] = xg + (size_t)(uint32_t)id[i] * GS;  // GS compile-time: one IMAD.WIDE.U32
     }
-    // shared leading members with this lane's previous edge (the run ids hold
-    // it); warp minimum, 0 on a tile's first step
-    int h = 0;
-    if constexpr (K > 3 && STTSV_MEMO) {
-      if (r > 0) {
-        int hl = 0;
-#pragma unroll
-        for (int i = 0; i < K - 3 && i < RMAX; ++i)
-          if (hl == i && id[i] == ra.rid[i]) hl = i + 1;
-        h = __reduce_min_sync(kFull, hl);
-      }
-    }
     const double w = sw[col];
     double q[K], F;
-#if STTSV_LEAN
-    dp_edge_lean<K, L>(rows, q, F);
-#else
-    dp_edge_table<K, L>(rows, P, STTSV_MEMO ? h : 0, q, F);
-#endif
+    dp_edge_table<K, L>(rows, q, F);
     const double wF = w * F;
     double dv[K];
 #pragma unroll
