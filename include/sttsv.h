@@ -143,8 +143,8 @@ sttsv_status_t sttsv_power_iterate(sttsv_plan_t plan, double* x_dev, double* z_d
  *            z = B x^{N-1}                          (line 7)
  *            lambda_min = min(z ./ x^[N-1]),  lambda_max = max(z ./ x^[N-1])   (lines 8-9)
  *   until (lambda_max - lambda_min) / lambda_min < tau  or  max_iters repetitions.
- * Min/max run over vertices with x_v > 0 (reading A15 of DESIGN.md: isolated
- * vertices have x_v = 0).  On return x_dev (device fp64[n]) holds x, z_dev
+ * Min/max run over vertices with x_v^(N-1) > 0 (reading A15 of DESIGN.md:
+ * isolated vertices have x_v = 0; powers that underflow are excluded).  On return x_dev (device fp64[n]) holds x, z_dev
  * (device fp64[n] or NULL) the last z, *lambda_min / *lambda_max the last
  * bracket and *iters_done the repetitions run.  Synchronous: the host reads the
  * bracket after every repetition.  tau >= 0 (0 runs exactly max_iters);

@@ -99,8 +99,9 @@ __global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __r
   }
 }
 
-// Alg. 1 lines 8-9: lambda_min/max of z ./ x^[N-1] over x > 0
-// (reading A15: isolated vertices, x = 0, are excluded).  Per-block partials,
+// Alg. 1 lines 8-9: lambda_min/max of z ./ x^[N-1] over the
+// vertices with x^[N-1] > 0 (reading A15: isolated vertices, x = 0, and
+// underflowed powers are excluded).  Per-block partials,
 // then one block combines them.
 __global__ void __launch_bounds__(kNormBlock) lambda_partial_kernel(const double* __restrict__ z,
                                                                    const double* __restrict__ x,
@@ -110,9 +111,9 @@ __global__ void __launch_bounds__(kNormBlock) lambda_partial_kernel(const double
   double lo = INFINITY, hi = -INFINITY;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double xv = x[i];
-    if (xv > 0.0) {
-      double p = 1.0;
-      for (int j = 0; j < Nm1; ++j) p *= xv;
+    double p = 1.0;
+    for (int j = 0; j < Nm1; ++j) p *= xv;
+    if (p > 0.0) {  // x_v^[N-1] > 0: x_v > 0 and no underflow (reading A15)
       const double r = z[i] / p;
       lo = fmin(lo, r);
       hi = fmax(hi, r);
