@@ -65,6 +65,10 @@ __device__ unsigned long long g_wait_cycles[4];
 #endif
 // ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
 // path: runtime member loop, prefix stack in shared memory (edge_big below)
+// two interleaved edges per lane step (ILP) in the small-rank kernel
+#ifndef STTSV_PAIR
+#define STTSV_PAIR 0
+#endif
 #ifndef STTSV_BIG_MIN
 #define STTSV_BIG_MIN 13
 #endif
@@ -218,9 +222,42 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
   constexpr int L = N - K + 1;
   constexpr int GS = series_stride(N);
   const int col0 = base + lane * EPL;
+#if STTSV_PAIR
+  // two consecutive edges per step: two independent DP chains in one basic block
+  // (instruction-level parallelism for the scheduler), deposited in order
+#pragma unroll 1
+  for (int r = 0; r + 1 < EPL; r += 2) {
+    const int ca = col0 + r, cb = ca + 1;
+    int ia[K], ib[K];
+    const double *ra_[K], *rb_[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      ia[i] = sids[i * TILE + ca];
+      ib[i] = sids[i * TILE + cb];
+      ra_[i] = xg + (size_t)(uint32_t)ia[i] * GS;
+      rb_[i] = xg + (size_t)(uint32_t)ib[i] * GS;
+    }
+    const double wa = sw[ca], wb = sw[cb];
+    double qa[K], qb[K], Fa, Fb;
+    dp_edge_table<K, L>(ra_, qa, Fa);
+    dp_edge_table<K, L>(rb_, qb, Fb);
+    const double wFa = wa * Fa, wFb = wb * Fb;
+    double da[K], db[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      da[i] = fma(wa, qa[i], wFa);
+      db[i] = fma(wb, qb[i], wFb);
+    }
+    slots_deposit<K, RMAX>(ia, da, ra, sk);
+    slots_deposit<K, RMAX>(ib, db, ra, sk);
+  }
+  if constexpr (EPL % 2 == 1) {
+    const int col = col0 + EPL - 1;
+#else
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
     const int col = col0 + r;
+#endif
     int id[K];
     const double* rows[K];
 #pragma unroll
