@@ -65,6 +65,10 @@ __device__ unsigned long long g_wait_cycles[4];
 #endif
 // ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
 // path: runtime member loop, prefix stack in shared memory (edge_big below)
+// consumer warps of the unrolled kernel for N = 11..(BIG_MIN-1)
+#ifndef STTSV_NCW_MID
+#define STTSV_NCW_MID 11
+#endif
 // two interleaved edges per lane step (ILP) in the small-rank kernel
 #ifndef STTSV_PAIR
 #define STTSV_PAIR 0
@@ -94,7 +98,7 @@ struct EdgeCfg {
   // when two stages of the largest bucket would not fit the ring budget; the
   // large-rank path runs 4 (2 for the generic kernel) register-heavy warps
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
-  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 10 ? STTSV_NCW_SMALL : 7);
+  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 10 ? STTSV_NCW_SMALL : STTSV_NCW_MID);
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
