@@ -308,6 +308,31 @@ def run_ours(args):
                   "note": "STTSV_MERGE_DUPLICATES plan (input incidences / time); not the headline"}
         mplan.close()
 
+    # ---------------- secondary: f4 batched apply (4 vectors share one pass over the edge stream)
+    batch = None
+    if not args.no_batch_report:
+        nv = 4
+        X = x.unsqueeze(0).repeat(nv, 1)
+        Y = torch.empty_like(X)
+        for _ in range(args.warmup):
+            plan.apply_batch(X, Y, stream)
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            plan.apply_batch(X, Y, stream)
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        bms = b0.elapsed_time(b1) / args.steps
+        if world > 1:
+            t = torch.tensor([bms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bms = t.item()
+        batch = {"vectors": nv, "value": nv * hg.incidences / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms,
+                 "note": "sttsv_apply_batch (SURVEY.md f4): vector-incidences/s; not the headline"}
+        del X, Y
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, dt, desc, threads, _ = oracle_sample(hg, args.cpu_seconds)
@@ -327,7 +352,7 @@ def run_ours(args):
                           "kernel_grid": info["kernel_grid"], "kernel_block": info["kernel_block"],
                           "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
                           / (ms_step * 1e-3) / 1e9},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "merge_duplicates": merged,
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "merge_duplicates": merged, "batch": batch,
                "gpu_launches": plan.launches() * args.steps, "clocks": sampler.summary()}
         print(json.dumps(out), flush=True)
     plan.close()
@@ -348,6 +373,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merge-report", action="store_true")
+    ap.add_argument("--no-batch-report", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: raising --warmup to 3 (timing rule)")

@@ -123,6 +123,19 @@ sttsv_status_t sttsv_plan_destroy(sttsv_plan_t plan);
  * With a comm the result is identical on all ranks (allreduce semantics). */
 sttsv_status_t sttsv_apply(sttsv_plan_t plan, const double* x_dev, double* y_dev, void* stream);
 
+/* sttsv_apply_batch — Y_v = B X_v^{N-1} for nvec vectors at once (SURVEY.md
+ * §8(f) f4: the hyperedge stream is read once for all vectors; each vector's
+ * DP and scatter run in turn on the staged tile).
+ *  X_dev  device fp64, vector v at X_dev + v*ld (length n), read only.
+ *  Y_dev  device fp64, same layout, overwritten; must not overlap X_dev.
+ *  nvec   1 .. STTSV_MAX_BATCH;  ld >= n.
+ * Stream-ordered like sttsv_apply; the first call with a larger nvec allocates a
+ * workspace (and synchronises the stream).  With a comm: one allreduce of all
+ * vectors' active parts.  Errors: INVALID_ARGUMENT, ALIAS, CUDA, NCCL, OUT_OF_MEMORY. */
+#define STTSV_MAX_BATCH 16
+sttsv_status_t sttsv_apply_batch(sttsv_plan_t plan, const double* X_dev, double* Y_dev, int nvec, int64_t ld,
+                                 void* stream);
+
 /* sttsv_apply_host — the same product from HOST vectors: copies x (fp64[n])
  * to the device, applies, copies y (fp64[n]) back, and synchronises before
  * returning.  Host buffers may be pageable; pinned buffers are faster. */

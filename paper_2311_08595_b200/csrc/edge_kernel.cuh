@@ -65,6 +65,10 @@ __device__ unsigned long long g_wait_cycles[4];
 #endif
 // ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
 // path: runtime member loop, prefix stack in shared memory (edge_big below)
+// L1 prefetch of the next member's table row in the large-rank path
+#ifndef STTSV_BIG_PREFETCH
+#define STTSV_BIG_PREFETCH 0
+#endif
 // consumer warps of the unrolled kernel for N = 11..(BIG_MIN-1)
 #ifndef STTSV_NCW_MID
 #define STTSV_NCW_MID 11
@@ -186,6 +190,34 @@ struct Sink {
 __device__ __forceinline__ void red_add(double* a, double d) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(d) : "memory");
 }
+// Warp-cooperative flush: lanes with v >= 0 hold a value d for vertex v.
+// Reduce over runs of equal adjacent v (v < 0 breaks runs); each run's first
+// lane deposits the run total with one red.  Whole warp.
+__device__ __forceinline__ void warp_flush(int v, double d, int lane, const Sink& sk) {
+  const int v0 = __shfl_sync(kFull, v, 0);
+  if (__all_sync(kFull, v == v0)) {
+    if (v0 < 0) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
+    if (lane == 0) red_add(sk.at(v0), d);
+    return;
+  }
+  // segmented suffix scan: a lane ends with the sum from itself to the end of its run
+  const int vn = __shfl_down_sync(kFull, v, 1);
+  int f = (lane == 31) || (vn != v);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double dn = __shfl_down_sync(kFull, d, o);
+    const int fn = __shfl_down_sync(kFull, f, o);
+    if (!f && lane + o < 32) {
+      d += dn;
+      f = fn;
+    }
+  }
+  const int vp = __shfl_up_sync(kFull, v, 1);
+  if ((lane == 0 || vp != v) && v >= 0) red_add(sk.at(v), d);
+}
+
 template <int RMAX>
 struct RunAcc {
   int rid[RMAX];
@@ -205,7 +237,7 @@ __device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (
       const int j = i < RMAX ? i : R1;  // compile-time after unrolling
       const bool fl = id[i] != ra.rid[j];
       if (fl) {  // rare: a branch (computing the address every step costs more)
-        red_add(sk.at(ra.rid[j]), ra.run[j]);
+        if (ra.rid[j] >= 0) red_add(sk.at(ra.rid[j]), ra.run[j]);
         ra.rid[j] = id[i];
         ra.run[j] = 0.0;
       }
@@ -300,6 +332,15 @@ __device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const dou
 // each member's series row is (re)loaded from the L1/L2-resident table where
 // it is used.  Products are formed in place (descending coefficient order).
 
+// L1 prefetch of a table row's first L coefficients (one instruction per 128-B line)
+template <int L>
+__device__ __forceinline__ void prefetch_row(const double* row) {
+#if STTSV_BIG_PREFETCH
+#pragma unroll
+  for (int j = 0; j < L; j += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + j));
+#endif
+}
+
 // a = (a*b) mod t^L, in place
 template <int L>
 __device__ __forceinline__ void trunc_mul_inplace(double (&a)[L], const double (&b)[L]) {
@@ -321,7 +362,7 @@ __device__ __forceinline__ void dep_slot(int i, int v, double d, RunAcc<RB>& ra,
     for (int r = 0; r < RB; ++r) {
       if (i == r) {
         if (v != ra.rid[r]) {
-          red_add(sk.at(ra.rid[r]), ra.run[r]);
+          if (ra.rid[r] >= 0) red_add(sk.at(ra.rid[r]), ra.run[r]);
           ra.rid[r] = v;
           ra.run[r] = 0.0;
         }
@@ -361,14 +402,17 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
     return;
   }
   double cur[L], g[L], S[L];
+  prefetch_row<L>(row(1));
   load_series<L>(row(0), cur);  // P_0
 #pragma unroll 1
   for (int i = 1; i <= K - 3; ++i) {
 #pragma unroll
     for (int j = 0; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push P_{i-1}
     load_series<L>(row(i), g);
+    prefetch_row<L>(row(i + 1));
     trunc_mul_inplace<L>(cur, g);  // P_i
   }
+  prefetch_row<L>(row(K - 1));
   // cur = P_{K-3}
   load_series<L>(row(K - 2), g);
   load_series<L>(row(K - 1), S);
@@ -386,6 +430,7 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
     for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
     dep_slot<RB>(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF), ra, sk);
     load_series<L>(row(i), g);
+    if (i > 1) prefetch_row<L>(row(i - 1));
     if (i > 1) {
       trunc_mul_inplace<L>(S, g);  // S_i = g_i S_{i+1}
     } else {
@@ -409,7 +454,9 @@ __device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid
 
 // ------------------------------------------------------------- the kernel
 // N == 0 is the generic instantiation (any rank <= STTSV_MAX_RANK).
-template <int N>
+// BATCH = false: one vector (sttsv_apply; runs continue across tiles);
+// BATCH = true: p.nvec vectors per tile (sttsv_apply_batch, f4).
+template <int N, bool BATCH>
 __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     edge_kernel(const __grid_constant__ EdgeKernelParams p) {
   using Cfg = EdgeCfg<N>;
@@ -420,12 +467,15 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   // stacks [p.stack_doubles][NCW*32] f64, thread-interleaved
   unsigned char* ring = smem_raw;
   double* stack = reinterpret_cast<double*>(smem_raw + STAGES * Cfg::STAGE_BYTES);
-  const Sink sk{p.priv + (size_t)blockIdx.x * p.H, p.ya, p.H};
+  // batch (f4): vector v uses xg + v*xg_vstride, ya + v*ya_vstride, priv slice + v*H
+  const int nvec = BATCH ? p.nvec : 1;
+  double* const priv_cta = p.priv + (size_t)blockIdx.x * p.H * nvec;
+  const Sink sk{priv_cta, p.ya, p.H};
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int64_t stile[STAGES];  // tile index staged in each slot (-1: no more work)
 
-  for (int j = tid; j < p.H; j += Cfg::THREADS) sk.priv[j] = 0.0;
+  for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) priv_cta[j] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -474,7 +524,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     RunAcc<RMAX> ra;
 #pragma unroll
     for (int i = 0; i < RMAX; ++i) {
-      ra.rid[i] = 0;  // flushing (0, 0.0) is a no-op deposit
+      ra.rid[i] = -1;  // empty run
       ra.run[i] = 0.0;
     }
     int b = 0;
@@ -502,16 +552,30 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
         const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
-        if constexpr (!Cfg::BIG) {
-          dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, p.xg, ra, sk, lane);
-        } else {
-          const int col = warp * 32 + lane;  // EPL = 1
+        // one pass per vector; with several vectors the runs of a pass are flushed
+        // (warp-aggregated) at its end, with one they continue across tiles
+        for (int v = 0; v < nvec; ++v) {
+          const Sink skv{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H};
+          const double* xgv = p.xg + (size_t)v * p.xg_vstride;
+          if constexpr (!Cfg::BIG) {
+            dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, xgv, ra, skv, lane);
+          } else {
+            const int col = warp * 32 + lane;  // EPL = 1
 #if STTSV_BIG_LOCAL
-          dispatch_big<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, sids + col, sw[col], p.xg, p.gs, lstk, ra, sk);
+            dispatch_big<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs, lstk, ra, skv);
 #else
-          dispatch_big<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, sids + col, sw[col], p.xg, p.gs,
-                                                      stack + (warp * 32 + lane), ra, sk);
+            dispatch_big<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs,
+                                                        stack + (warp * 32 + lane), ra, skv);
 #endif
+          }
+          if constexpr (BATCH) {
+#pragma unroll
+            for (int i = 0; i < RMAX; ++i) {
+              warp_flush(ra.rid[i], ra.run[i], lane, skv);
+              ra.rid[i] = -1;
+              ra.run[i] = 0.0;
+            }
+          }
         }
       }
       __syncwarp();
@@ -524,20 +588,20 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
       atomicAdd(&g_wait_cycles[2], 1ull);
     }
 #endif
-    // flush the run accumulators
-    if (any) {
+    // flush the run accumulators (single-vector mode)
+    if (any && !BATCH) {
 #pragma unroll
       for (int i = 0; i < RMAX; ++i)
-        if (ra.run[i] != 0.0) red_add(sk.at(ra.rid[i]), ra.run[i]);
+        if (ra.rid[i] >= 0 && ra.run[i] != 0.0) red_add(sk.at(ra.rid[i]), ra.run[i]);
     }
   }
   // this CTA's reds into priv are ordered before the reads below (fence + barrier);
   // the reads go to L2 (ld.cg), where the reds were performed
   __threadfence();
   __syncthreads();
-  for (int j = tid; j < p.H; j += Cfg::THREADS) {
-    const double v = __ldcg(sk.priv + j);
-    if (v != 0.0) red_add(p.ya + j, v);
+  for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) {
+    const double v = __ldcg(priv_cta + j);
+    if (v != 0.0) red_add(p.ya + (size_t)(j / p.H) * p.ya_vstride + j % p.H, v);
   }
 }
 

@@ -39,7 +39,10 @@ struct EdgeKernelParams {
   const double* xg;      // series table: row i = g[j] = x_a[i]^{j+1}/(j+1)!, j < gs (dp.cuh)
   int32_t gs;            // row stride of xg (doubles, even)
   double* ya;            // y on active vertices (accumulated)
-  double* priv;          // [grid][H] per-CTA accumulators of the hot ids (zeroed by the kernel)
+  double* priv;          // [grid][nvec][H] per-CTA accumulators of the hot ids (zeroed by the kernel)
+  int32_t nvec;          // vectors per apply (f4 batch; 1 = sttsv_apply)
+  int64_t xg_vstride;    // doubles between the series tables of consecutive vectors
+  int64_t ya_vstride;    // doubles between the y_a of consecutive vectors
   int32_t n_active;
   int32_t T;             // slots with a per-lane register run accumulator (informational)
   int32_t H;             // ids < H accumulate in the CTA's private slice of priv
@@ -55,7 +58,8 @@ struct EdgeKernelParams {
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(25)
 
 struct EdgeKernelEntry {
-  const void* fn;      // __global__ edge_kernel<N>
+  const void* fn;       // __global__ edge_kernel<N, false> (one vector)
+  const void* fn_batch; // __global__ edge_kernel<N, true> (sttsv_apply_batch)
   int block;           // threads per CTA (consumer warps + one producer warp)
   int tile;            // edges per tile
   size_t ring_bytes;   // shared memory of the TMA ring
@@ -77,7 +81,7 @@ size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N);
 int edge_big_stack_doubles(int N);
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
-                               cudaStream_t s);
+                               cudaStream_t s, bool batch = false);
 cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
                           cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);

@@ -184,13 +184,15 @@ size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N) {
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm) {
   cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(e.fn_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(max_blocks_per_sm, e.fn, e.block, smem);
 }
 
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool batch) {
   void* args[] = {const_cast<EdgeKernelParams*>(&p)};
-  return cudaLaunchKernel(e.fn, dim3(grid), dim3(e.block), args, smem, s);
+  return cudaLaunchKernel(batch ? e.fn_batch : e.fn, dim3(grid), dim3(e.block), args, smem, s);
 }
 
 static int grid_for(int64_t n, int block, int cap) {

@@ -224,6 +224,10 @@ struct sttsv_plan_s {
   double* d_yhost = nullptr;
   cudaStream_t host_stream = nullptr;
   double* h_lambda = nullptr;  // pinned (lambda_min, lambda_max) of sttsv_hec
+  // batch (f4) workspace, grown on demand by sttsv_apply_batch
+  int batch_cap = 0;
+  void* batch_mem = nullptr;
+  double *b_xa = nullptr, *b_xg = nullptr, *b_ya = nullptr, *b_priv = nullptr;
   // kernel
   EdgeKernelEntry ent{};
   EdgeKernelParams kp{};
@@ -295,6 +299,7 @@ static void free_plan(sttsv_plan_s* p) {
   if (p->d_xhost) cudaFree(p->d_xhost);
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
   if (p->h_lambda) cudaFreeHost(p->h_lambda);
+  if (p->batch_mem) cudaFree(p->batch_mem);
   delete p;
 }
 
@@ -579,6 +584,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.gs = gs;
   kp.ya = p->d_ya;
   kp.tile_counter = d_cnt;
+  kp.nvec = 1;
+  kp.xg_vstride = (int64_t)na * gs;
+  kp.ya_vstride = na;
   kp.priv = d_priv;
 
   p->grid = (int)grid;
@@ -793,5 +801,63 @@ extern "C" sttsv_status_t sttsv_hec(sttsv_plan_t p, double* x, double* z, double
   *lambda_min = lo;
   *lambda_max = hi;
   *iters_done = it;
+  return STTSV_OK;
+}
+
+extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, double* Y, int nvec, int64_t ld,
+                                            void* stream) {
+  if (!p || !X || !Y) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (nvec < 1 || nvec > STTSV_MAX_BATCH) return fail(STTSV_ERR_INVALID_ARGUMENT, "nvec must be in [1, %d]", STTSV_MAX_BATCH);
+  if (ld < p->n) return fail(STTSV_ERR_INVALID_ARGUMENT, "ld < n");
+  const size_t span = ((size_t)(nvec - 1) * (size_t)ld + (size_t)p->n) * sizeof(double);
+  if (overlap(X, span, Y, span)) return fail(STTSV_ERR_ALIAS, "X and Y overlap");
+  DeviceGuard g(p->device);
+  sttsv_status_t st = check_async(p);
+  if (st != STTSV_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t na = p->n_active;
+  if (p->batch_cap < nvec) {
+    CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+    if (p->batch_mem) CUDA_TRY(cudaFree(p->batch_mem), "cudaFree batch");
+    p->batch_mem = nullptr;
+    p->batch_cap = 0;
+    const size_t a = ((size_t)nvec * na * 8 + 255) & ~(size_t)255;
+    const size_t gbytes = ((size_t)nvec * na * p->gs * 8 + 255) & ~(size_t)255;
+    const size_t pr = (size_t)p->grid * p->kp.H * nvec * 8 + 8;
+    CUDA_TRY(cudaMalloc(&p->batch_mem, 2 * a + gbytes + pr), "cudaMalloc batch workspace");
+    char* b = (char*)p->batch_mem;
+    p->b_xa = (double*)b;
+    p->b_ya = (double*)(b + a);
+    p->b_xg = (double*)(b + 2 * a);
+    p->b_priv = (double*)(b + 2 * a + gbytes);
+    p->batch_cap = nvec;
+  }
+  for (int v = 0; v < nvec; ++v)
+    CUDA_TRY(launch_gather(X + (size_t)v * ld, p->d_act, p->b_xa + (size_t)v * na, p->b_xg + (size_t)v * na * p->gs,
+                           p->gs, na, s), "gather launch");
+  if (na > 0) {
+    CUDA_TRY(cudaMemsetAsync(p->b_ya, 0, (size_t)nvec * na * sizeof(double), s), "memset y_a");
+    if (p->kp.num_tiles > 0) {
+      EdgeKernelParams kp = p->kp;
+      kp.nvec = nvec;
+      kp.xa = p->b_xa;
+      kp.xg = p->b_xg;
+      kp.xg_vstride = na * p->gs;
+      kp.ya = p->b_ya;
+      kp.ya_vstride = na;
+      kp.priv = p->b_priv;
+      CUDA_TRY(cudaMemsetAsync(kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
+      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1), "edge kernel launch");
+    }
+    if (p->comm && p->world > 1) {
+      NcclApi* api = nccl_api();
+      ncclResult_t r = api->AllReduce(p->b_ya, p->b_ya, (size_t)nvec * na, ncclFloat64, ncclSum, p->comm->comm, s);
+      if (r != ncclSuccess) return fail(STTSV_ERR_NCCL, "ncclAllReduce: %s", api->GetErrorString(r));
+    }
+  }
+  for (int v = 0; v < nvec; ++v) {
+    CUDA_TRY(cudaMemsetAsync(Y + (size_t)v * ld, 0, (size_t)p->n * sizeof(double), s), "memset Y");
+    CUDA_TRY(launch_expand(p->b_ya + (size_t)v * na, p->d_act, Y + (size_t)v * ld, na, s), "expand launch");
+  }
   return STTSV_OK;
 }

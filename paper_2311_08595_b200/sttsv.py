@@ -70,6 +70,7 @@ def load():
         "sttsv_plan_destroy": ([P], st),
         "sttsv_apply": ([P, P, P, P], st),
         "sttsv_apply_host": ([P, P, P], st),
+        "sttsv_apply_batch": ([P, P, P, ctypes.c_int, i64, P], st),
         "sttsv_power_iterate": ([P, P, P, ctypes.c_int, P], st),
         "sttsv_hec": ([P, P, P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), P], st),
@@ -94,7 +95,8 @@ def load():
 
 
 def exported_symbols() -> list[str]:
-    return ["sttsv_plan_create", "sttsv_plan_destroy", "sttsv_apply", "sttsv_apply_host", "sttsv_power_iterate",
+    return ["sttsv_plan_create", "sttsv_plan_destroy", "sttsv_apply", "sttsv_apply_host", "sttsv_apply_batch",
+            "sttsv_power_iterate",
             "sttsv_hec",
             "sttsv_plan_info", "sttsv_apply_launches", "sttsv_plan_profile", "sttsv_plan_profile_read",
             "sttsv_shard_edges", "sttsv_comm_unique_id",
@@ -141,6 +143,12 @@ def sttsv_plan_destroy(plan):
 
 def sttsv_apply(plan, x_dev, y_dev, stream=None, device=None):
     _check(load().sttsv_apply(plan, _ptr(x_dev), _ptr(y_dev), _stream_ptr(stream, device or x_dev.device)))
+
+
+def sttsv_apply_batch(plan, X_dev, Y_dev, stream=None):
+    """X_dev, Y_dev: (nvec, ld) float64 CUDA tensors, rows are vectors (ld >= n)."""
+    _check(load().sttsv_apply_batch(plan, _ptr(X_dev), _ptr(Y_dev), int(X_dev.shape[0]), int(X_dev.stride(0)),
+                                    _stream_ptr(stream, X_dev.device)))
 
 
 def sttsv_apply_host(plan, x_host: np.ndarray, y_host: np.ndarray):
@@ -258,6 +266,19 @@ class Plan:
         self._check_vec(y)
         sttsv_apply(self._h, x, y, stream)
         return y
+
+    def apply_batch(self, X, Y=None, stream=None):
+        """Y[v] = B X[v]^{N-1} for the rows of X (nvec x n float64 CUDA tensor)."""
+        import torch
+        if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float64 and X.dim() == 2
+                and X.shape[1] == self.n and X.stride(1) == 1 and X.device.index == self.device):
+            raise ValueError("X must be a (nvec, n) float64 CUDA tensor with unit column stride")
+        if Y is None:
+            Y = torch.empty_strided(tuple(X.shape), X.stride(), dtype=X.dtype, device=X.device)
+        if Y.shape != X.shape or Y.stride() != X.stride():
+            raise ValueError("Y must have X's shape and strides")
+        sttsv_apply_batch(self._h, X, Y, stream)
+        return Y
 
     def apply_host(self, x: np.ndarray, y: np.ndarray | None = None) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)

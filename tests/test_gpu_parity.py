@@ -286,3 +286,25 @@ def test_hec_matches_oracle(S, torch_cuda):
     assert abs(it - it_o) <= 3, (it, it_o)
     assert rel(x.cpu().numpy(), xo) < 1e-8    # both within the converged bracket
     plan.close()
+
+
+@pytest.mark.parametrize("name,m,n,nvec", [("tiny", None, None, 3), ("mid", 100_000, None, 4),
+                                           ("large", 200_000, 1_000_000, 2), ("high-rank", 800, None, 3),
+                                           ("centrality", 50_000, None, 5)])
+def test_apply_batch(S, torch_cuda, name, m, n, nvec):
+    """f4: Y_v = B X_v^{N-1} for several vectors sharing one pass over the edge stream."""
+    torch = torch_cuda
+    hg = W.generate(name, m=m, n=n)
+    plan = S.Plan.from_hypergraph(hg)
+    rng = np.random.default_rng(nvec)
+    ld = hg.n + 7                                   # padded rows
+    Xh = rng.uniform(0.05, 1.0, size=(nvec, ld))
+    X = torch.from_numpy(Xh).cuda()[:, :hg.n]
+    Y = plan.apply_batch(X)
+    torch.cuda.synchronize()
+    Yh = Y.cpu().numpy()
+    for v in range(nvec):
+        assert rel(Yh[v], oracle.sttsv(hg, x=Xh[v, :hg.n])) < TOL, (name, v)
+    y1 = plan.apply(X[1].contiguous())              # the single-vector path agrees
+    assert rel(y1.cpu().numpy(), Yh[1]) < 1e-13
+    plan.close()
