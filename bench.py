@@ -375,6 +375,10 @@ def main():
     ap.add_argument("--no-merge-report", action="store_true")
     ap.add_argument("--no-batch-report", action="store_true")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # one process per GPU: share the host cores among the ranks' generators/planners
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or world) // world))
     if args.warmup < 3 and args.impl == "ours":
         log("note: raising --warmup to 3 (timing rule)")
         args.warmup = 3

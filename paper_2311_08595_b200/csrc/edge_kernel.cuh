@@ -75,6 +75,10 @@ __device__ unsigned long long g_wait_cycles[4];
 #ifndef STTSV_BIG_PREFETCH
 #define STTSV_BIG_PREFETCH 0
 #endif
+// CTAs per SM of the unrolled kernel for N = 11..(BIG_MIN-1)
+#ifndef STTSV_MID_BLOCKS
+#define STTSV_MID_BLOCKS 1
+#endif
 // consumer warps of the unrolled kernel for N = 11..(BIG_MIN-1)
 #ifndef STTSV_NCW_MID
 #define STTSV_NCW_MID 11
@@ -103,7 +107,8 @@ struct EdgeCfg {
   static constexpr int EDGE_BYTES = 4 * KMAX + 8;           // staged bytes per edge (ids + w')
   // dynamic shared memory for the TMA ring (<= 227 KB in total; the large-rank
   // path also needs its prefix stack)
-  static constexpr int RING_BUDGET = BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024 : (N <= 10 ? STTSV_RING_KB : 220) * 1024;
+  static constexpr int RING_BUDGET =
+      BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024 : (N <= 10 ? STTSV_RING_KB : 220 / STTSV_MID_BLOCKS) * 1024;
   // consumer warps: 15 (+1 producer = 4 warps per SMSP) for small ranks; fewer
   // when two stages of the largest bucket would not fit the ring budget; the
   // large-rank path runs 4 (2 for the generic kernel) register-heavy warps
@@ -116,7 +121,7 @@ struct EdgeCfg {
   static constexpr int STAGES_FIT = RING_BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
   static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
-  static constexpr int MIN_BLOCKS = (!BIG && N <= 10) ? STTSV_MIN_BLOCKS : 1;
+  static constexpr int MIN_BLOCKS = BIG ? 1 : (N <= 10 ? STTSV_MIN_BLOCKS : STTSV_MID_BLOCKS);
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
 };
