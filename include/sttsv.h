@@ -72,7 +72,10 @@ enum {
                                        repeated ids are still an error                             */
   STTSV_MERGE_DUPLICATES = 1u << 1, /* merge identical vertex sets of a shard, summing their weights
                                        (B is linear in w); the plan stores fewer edges */
-  STTSV_DETERMINISTIC = 1u << 2     /* reserved (NEXT f2): bit-reproducible reduction order          */
+  STTSV_DETERMINISTIC = 1u << 2     /* bit-reproducible y: each contribution is stored to a
+                                       plan-time slot of a vertex-major buffer and summed in a fixed order
+                                       (no atomics); costs ~12 B more per incidence per apply, needs
+                                       < 2^31 incidences per shard; not with sttsv_apply_batch nvec > 1 */
 };
 
 /* ------------------------------------------------------------------ plans */
@@ -99,8 +102,7 @@ enum {
  *            world/rank: sttsv_apply then all-reduces the active part of y
  *            over NCCL so every rank returns the full s.  With world > 1 and
  *            comm == NULL, sttsv_apply returns only this shard's partial sum.
- *  flags     STTSV_CANONICALIZE, STTSV_MERGE_DUPLICATES; STTSV_DETERMINISTIC (reserved)
- *            returns STTSV_ERR_UNSUPPORTED.
+ *  flags     STTSV_CANONICALIZE, STTSV_MERGE_DUPLICATES, STTSV_DETERMINISTIC.
  *
  * The host arrays are copied; the caller may free them on return.  The plan
  * owns all its device memory until sttsv_plan_destroy.  A plan is immutable

@@ -13,8 +13,9 @@
 namespace sttsv {
 EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   EdgeKernelEntry e;
-  e.fn = (const void*)edge_kernel<STTSV_INST_N, false>;
-  e.fn_batch = (const void*)edge_kernel<STTSV_INST_N, true>;
+  e.fn = (const void*)edge_kernel<STTSV_INST_N, false, false>;
+  e.fn_batch = (const void*)edge_kernel<STTSV_INST_N, true, false>;
+  e.fn_det = (const void*)edge_kernel<STTSV_INST_N, false, true>;
   e.block = EdgeCfg<STTSV_INST_N>::THREADS;
   e.tile = EdgeCfg<STTSV_INST_N>::TILE;
   e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::STAGES * EdgeCfg<STTSV_INST_N>::STAGE_BYTES;

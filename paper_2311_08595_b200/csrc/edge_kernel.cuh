@@ -83,10 +83,6 @@ __device__ unsigned long long g_wait_cycles[4];
 #ifndef STTSV_NCW_MID
 #define STTSV_NCW_MID 11
 #endif
-// two interleaved edges per lane step (ILP) in the small-rank kernel
-#ifndef STTSV_PAIR
-#define STTSV_PAIR 0
-#endif
 #ifndef STTSV_BIG_MIN
 #define STTSV_BIG_MIN 13
 #endif
@@ -232,6 +228,17 @@ struct RunAcc {
   double run[RMAX];
 };
 
+// Deterministic mode (STTSV_DETERMINISTIC): every incidence's
+// contribution is STORED to its plan-time slot of a vertex-major buffer
+// (contrib[slot]), no atomics; a second pass (kernels.cu det_reduce) sums each
+// vertex's segment in a fixed order.  The slot column of member i of the
+// tile's column c is slot[i * sstride + c].
+struct DetSink {
+  const int32_t* slot;  // this tile's slot columns (bucket slot pool + tile start)
+  int64_t sstride;      // column stride of the slot pool (= the bucket's id stride)
+  double* contrib;
+};
+
 // One step of a lane: slots (id[i], dv[i]) of its current edge.  Slot i <
 // RMAX: same vertex as the run -> add; else flush the run (one red) and start
 // a new one.  Slots >= RMAX: one red.
@@ -259,49 +266,16 @@ __device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (
 // The warp's block of a staged tile (size-K bucket): lane l takes the EPL
 // consecutive columns base + l*EPL + r, r = 0..EPL-1.  Buckets are padded to
 // whole tiles with weight-0 copies of their last edge, so every column is valid.
-template <int N, int K, int TILE, int EPL, int RMAX>
+template <int N, int K, int TILE, int EPL, int RMAX, bool DET>
 __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, const double* __restrict__ sw, int base,
                                            const double* __restrict__ xg, RunAcc<RMAX>& ra, const Sink& sk,
-                                           int lane) {
+                                           const DetSink& ds, int lane) {
   constexpr int L = N - K + 1;
   constexpr int GS = series_stride(N);
   const int col0 = base + lane * EPL;
-#if STTSV_PAIR
-  // two consecutive edges per step: two independent DP chains in one basic block
-  // (instruction-level parallelism for the scheduler), deposited in order
-#pragma unroll 1
-  for (int r = 0; r + 1 < EPL; r += 2) {
-    const int ca = col0 + r, cb = ca + 1;
-    int ia[K], ib[K];
-    const double *ra_[K], *rb_[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      ia[i] = sids[i * TILE + ca];
-      ib[i] = sids[i * TILE + cb];
-      ra_[i] = xg + (size_t)(uint32_t)ia[i] * GS;
-      rb_[i] = xg + (size_t)(uint32_t)ib[i] * GS;
-    }
-    const double wa = sw[ca], wb = sw[cb];
-    double qa[K], qb[K], Fa, Fb;
-    dp_edge_table<K, L>(ra_, qa, Fa);
-    dp_edge_table<K, L>(rb_, qb, Fb);
-    const double wFa = wa * Fa, wFb = wb * Fb;
-    double da[K], db[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      da[i] = fma(wa, qa[i], wFa);
-      db[i] = fma(wb, qb[i], wFb);
-    }
-    slots_deposit<K, RMAX>(ia, da, ra, sk);
-    slots_deposit<K, RMAX>(ib, db, ra, sk);
-  }
-  if constexpr (EPL % 2 == 1) {
-    const int col = col0 + EPL - 1;
-#else
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
     const int col = col0 + r;
-#endif
     int id[K];
     const double* rows[K];
 #pragma unroll
@@ -316,19 +290,25 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
     double dv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) dv[i] = fma(w, q[i], wF);
-    slots_deposit<K, RMAX>(id, dv, ra, sk);
+    if constexpr (DET) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) ds.contrib[__ldg(ds.slot + i * ds.sstride + col)] = dv[i];
+    } else {
+      slots_deposit<K, RMAX>(id, dv, ra, sk);
+    }
   }
 }
 
-template <int N, int K, int TILE, int EPL, int RMAX>
+template <int N, int K, int TILE, int EPL, int RMAX, bool DET>
 __device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int base,
-                                           const double* xg, RunAcc<RMAX>& ra, const Sink& sk, int lane) {
+                                           const double* xg, RunAcc<RMAX>& ra, const Sink& sk, const DetSink& ds,
+                                           int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      warp_block<N, K, TILE, EPL, RMAX>(sids, sw, base, xg, ra, sk, lane);
+      warp_block<N, K, TILE, EPL, RMAX, DET>(sids, sw, base, xg, ra, sk, ds, lane);
       return;
     }
-    dispatch_k<N, K + 1, TILE, EPL, RMAX>(k, sids, sw, base, xg, ra, sk, lane);
+    dispatch_k<N, K + 1, TILE, EPL, RMAX, DET>(k, sids, sw, base, xg, ra, sk, ds, lane);
   }
 }
 
@@ -385,17 +365,22 @@ __device__ __forceinline__ void dep_slot(int i, int v, double d, RunAcc<RB>& ra,
 // one edge of size K (runtime) with L = N-K+1 (compile time); sid = member 0's
 // id in the staged tile (member i at sid[i * TILE]); stk = this thread's stack
 // (row r coefficient j at stk[(r * L + j) * NT])
-template <int L, int TILE, int NT, int RB>
+template <int L, int TILE, int NT, int RB, bool DET>
 __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid, double w,
                                          const double* __restrict__ xg, int gs, double* __restrict__ stk,
-                                         RunAcc<RB>& ra, const Sink& sk) {
+                                         RunAcc<RB>& ra, const Sink& sk, const DetSink& ds, int col) {
   // NT = 1: stk is a thread-private (local) array; else thread-interleaved shared memory
   constexpr int D = L - 1;
   auto row = [&](int i) { return xg + (size_t)(uint32_t)sid[i * TILE] * gs; };
+  // deposit of member i's contribution (runs + reds, or the deterministic store)
+  auto dep = [&](int i, int v, double d) {
+    if constexpr (DET) ds.contrib[__ldg(ds.slot + i * ds.sstride + col)] = d;
+    else dep_slot<RB>(i, v, d, ra, sk);
+  };
   if (K == 1) {
     // singleton: Q = 1 (empty product), F = g_0:  q = [D == 0],  F[D-1] = x^D / D!
     const double F = D >= 1 ? __ldg(row(0) + (D >= 1 ? D - 1 : 0)) : 0.0;
-    dep_slot<RB>(0, sid[0], w * ((D == 0 ? 1.0 : 0.0) + F), ra, sk);
+    dep(0, sid[0], w * ((D == 0 ? 1.0 : 0.0) + F));
     return;
   }
   if (K == 2) {
@@ -405,8 +390,8 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
     double F = 0.0;
     if constexpr (D >= 1) F = coef<D - 1, L>(a, b);
     const double wF = w * F;
-    dep_slot<RB>(0, sid[0], fma(w, b[D], wF), ra, sk);
-    dep_slot<RB>(1, sid[TILE], fma(w, a[D], wF), ra, sk);
+    dep(0, sid[0], fma(w, b[D], wF));
+    dep(1, sid[TILE], fma(w, a[D], wF));
     return;
   }
   double cur[L], g[L], S[L];
@@ -430,33 +415,34 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
   double F = 0.0;
   if constexpr (D >= 1) F = coef<D - 1, L>(cur, S);
   const double wF = w * F;
-  dep_slot<RB>(K - 1, sid[(K - 1) * TILE], fma(w, qa, wF), ra, sk);
-  dep_slot<RB>(K - 2, sid[(K - 2) * TILE], fma(w, qb, wF), ra, sk);
+  dep(K - 1, sid[(K - 1) * TILE], fma(w, qa, wF));
+  dep(K - 2, sid[(K - 2) * TILE], fma(w, qb, wF));
 #pragma unroll 1
   for (int i = K - 3; i >= 1; --i) {
 #pragma unroll
     for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
-    dep_slot<RB>(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF), ra, sk);
+    dep(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF));
     load_series<L>(row(i), g);
     if (i > 1) prefetch_row<L>(row(i - 1));
     if (i > 1) {
       trunc_mul_inplace<L>(S, g);  // S_i = g_i S_{i+1}
     } else {
-      dep_slot<RB>(0, sid[0], fma(w, coef<D, L>(g, S), wF), ra, sk);  // [t^D] g_1 S_2
+      dep(0, sid[0], fma(w, coef<D, L>(g, S), wF));  // [t^D] g_1 S_2
     }
   }
-  if (K == 3) dep_slot<RB>(0, sid[0], fma(w, S[D], wF), ra, sk);  // S = S_1
+  if (K == 3) dep(0, sid[0], fma(w, S[D], wF));  // S = S_1
 }
 
-template <int L, int LMAX, int TILE, int NT, int RB>
+template <int L, int LMAX, int TILE, int NT, int RB, bool DET>
 __device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid, double w, const double* xg, int gs,
-                                             double* stk, RunAcc<RB>& ra, const Sink& sk) {
+                                             double* stk, RunAcc<RB>& ra, const Sink& sk, const DetSink& ds,
+                                             int col) {
   if constexpr (L <= LMAX) {
     if (L_rt == L) {
-      edge_big<L, TILE, NT, RB>(K, sid, w, xg, gs, stk, ra, sk);
+      edge_big<L, TILE, NT, RB, DET>(K, sid, w, xg, gs, stk, ra, sk, ds, col);
       return;
     }
-    dispatch_big<L + 1, LMAX, TILE, NT, RB>(L_rt, K, sid, w, xg, gs, stk, ra, sk);
+    dispatch_big<L + 1, LMAX, TILE, NT, RB, DET>(L_rt, K, sid, w, xg, gs, stk, ra, sk, ds, col);
   }
 }
 
@@ -464,7 +450,8 @@ __device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid
 // N == 0 is the generic instantiation (any rank <= STTSV_MAX_RANK).
 // BATCH = false: one vector (sttsv_apply; runs continue across tiles);
 // BATCH = true: p.nvec vectors per tile (sttsv_apply_batch, f4).
-template <int N, bool BATCH>
+// DET = true: deterministic stores into the vertex-major buffer (f2; one vector).
+template <int N, bool BATCH, bool DET>
 __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     edge_kernel(const __grid_constant__ EdgeKernelParams p) {
   using Cfg = EdgeCfg<N>;
@@ -556,6 +543,8 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
       any = true;
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
       const int k = p.b[b].k;
+      const DetSink ds{DET ? p.slot + p.b[b].ids_off + (t - p.b[b].tile_begin) * TILE : nullptr, p.b[b].stride,
+                       p.contrib};
       {
         const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
@@ -566,14 +555,15 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
           const Sink skv{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H};
           const double* xgv = p.xg + (size_t)v * p.xg_vstride;
           if constexpr (!Cfg::BIG) {
-            dispatch_k<N, 1, TILE, EPL, RMAX>(k, sids, sw, base, xgv, ra, skv, lane);
+            dispatch_k<N, 1, TILE, EPL, RMAX, DET>(k, sids, sw, base, xgv, ra, skv, ds, lane);
           } else {
             const int col = warp * 32 + lane;  // EPL = 1
 #if STTSV_BIG_LOCAL
-            dispatch_big<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs, lstk, ra, skv);
+            dispatch_big<1, KMAX, TILE, 1, RMAX, DET>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs, lstk, ra, skv,
+                                                      ds, col);
 #else
-            dispatch_big<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs,
-                                                        stack + (warp * 32 + lane), ra, skv);
+            dispatch_big<1, KMAX, TILE, NCW * 32, RMAX, DET>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs,
+                                                             stack + (warp * 32 + lane), ra, skv, ds, col);
 #endif
           }
           if constexpr (BATCH) {

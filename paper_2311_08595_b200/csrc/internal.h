@@ -43,6 +43,8 @@ struct EdgeKernelParams {
   int32_t nvec;          // vectors per apply (f4 batch; 1 = sttsv_apply)
   int64_t xg_vstride;    // doubles between the series tables of consecutive vectors
   int64_t ya_vstride;    // doubles between the y_a of consecutive vectors
+  const int32_t* slot;   // deterministic mode: slot pool (layout of ids) -> position in contrib
+  double* contrib;       // deterministic mode: vertex-major contributions
   int32_t n_active;
   int32_t T;             // slots with a per-lane register run accumulator (informational)
   int32_t H;             // ids < H accumulate in the CTA's private slice of priv
@@ -59,7 +61,8 @@ struct EdgeKernelParams {
 
 struct EdgeKernelEntry {
   const void* fn;       // __global__ edge_kernel<N, false> (one vector)
-  const void* fn_batch; // __global__ edge_kernel<N, true> (sttsv_apply_batch)
+  const void* fn_batch; // __global__ edge_kernel<N, true, false> (sttsv_apply_batch)
+  const void* fn_det;   // __global__ edge_kernel<N, false, true> (STTSV_DETERMINISTIC plans)
   int block;           // threads per CTA (consumer warps + one producer warp)
   int tile;            // edges per tile
   size_t ring_bytes;   // shared memory of the TMA ring
@@ -80,8 +83,14 @@ size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N);
 // doubles of prefix stack per consumer thread of the large-rank path (edge_kernel.cuh)
 int edge_big_stack_doubles(int N);
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
+// mode: 0 one vector, 1 batch, 2 deterministic
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
-                               cudaStream_t s, bool batch = false);
+                               cudaStream_t s, int mode = 0);
+// deterministic mode, pass 2: chunk sums (chunk c = contrib[cstart[c] .. cstart[c+1])) in a fixed
+// tree order, then y_a[v] = sum of v's chunks (vchunk[v] .. vchunk[v+1]) in order
+cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int64_t nchunks, double* csum,
+                              const int64_t* vchunk, double* ya, int64_t n_active, cudaStream_t s);
+constexpr int kDetChunk = 4096;  // contributions per deterministic reduction chunk
 cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
                           cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);

@@ -162,6 +162,40 @@ __global__ void lambda_final_kernel(const double* __restrict__ partial, int npar
   }
 }
 
+// Deterministic reduction (STTSV_DETERMINISTIC).  Each chunk (<= kDetChunk
+// consecutive contributions of ONE vertex) is summed by one CTA of 256 threads:
+// thread j adds elements j, j+256, ... in order, then a fixed shuffle/shared
+// tree; the result depends only on the data, never on scheduling.
+constexpr int kDetBlock = 256;
+__global__ void __launch_bounds__(kDetBlock) det_chunk_kernel(const double* __restrict__ contrib,
+                                                              const int64_t* __restrict__ cstart,
+                                                              double* __restrict__ csum) {
+  __shared__ double red[kDetBlock / 32];
+  const int64_t c = blockIdx.x;
+  const int64_t a = cstart[c], b = cstart[c + 1];
+  double s = 0.0;
+  for (int64_t i = a + threadIdx.x; i < b; i += kDetBlock) s += contrib[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kDetBlock / 32; ++w) t += red[w];
+    csum[c] = t;
+  }
+}
+
+__global__ void det_vertex_kernel(const double* __restrict__ csum, const int64_t* __restrict__ vchunk,
+                                  double* __restrict__ ya, int64_t n_active) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_active;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int64_t c = vchunk[v]; c < vchunk[v + 1]; ++c) t += csum[c];
+    ya[v] = t;
+  }
+}
+
 // ------------------------------------------------------------- launchers
 EdgeKernelEntry edge_entry(int N) {
   switch (N) {
@@ -186,13 +220,16 @@ cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_b
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(e.fn_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(e.fn_det, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(max_blocks_per_sm, e.fn, e.block, smem);
 }
 
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
-                               cudaStream_t s, bool batch) {
+                               cudaStream_t s, int mode) {
   void* args[] = {const_cast<EdgeKernelParams*>(&p)};
-  return cudaLaunchKernel(batch ? e.fn_batch : e.fn, dim3(grid), dim3(e.block), args, smem, s);
+  const void* fn = mode == 1 ? e.fn_batch : (mode == 2 ? e.fn_det : e.fn);
+  return cudaLaunchKernel(fn, dim3(grid), dim3(e.block), args, smem, s);
 }
 
 static int grid_for(int64_t n, int block, int cap) {
@@ -221,6 +258,13 @@ cudaError_t launch_lambda(const double* z, const double* x, double* partial, dou
   const int grid = grid_for(n_active, kNormBlock, kNormMaxGrid);
   lambda_partial_kernel<<<grid, kNormBlock, 0, s>>>(z, x, partial, n_active, N - 1);
   lambda_final_kernel<<<1, 32, 0, s>>>(partial, grid, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int64_t nchunks, double* csum,
+                              const int64_t* vchunk, double* ya, int64_t n_active, cudaStream_t s) {
+  if (nchunks > 0) det_chunk_kernel<<<(unsigned)nchunks, kDetBlock, 0, s>>>(contrib, cstart, csum);
+  if (n_active > 0) det_vertex_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(csum, vchunk, ya, n_active);
   return cudaGetLastError();
 }
 

@@ -224,6 +224,12 @@ struct sttsv_plan_s {
   double* d_yhost = nullptr;
   cudaStream_t host_stream = nullptr;
   double* h_lambda = nullptr;  // pinned (lambda_min, lambda_max) of sttsv_hec
+  // deterministic mode (STTSV_DETERMINISTIC): slot pool, vertex-major buffer, chunks
+  bool det = false;
+  void* det_mem = nullptr;
+  int64_t det_chunks = 0;
+  double *d_contrib = nullptr, *d_csum = nullptr;
+  int64_t *d_cstart = nullptr, *d_vchunk = nullptr;
   // batch (f4) workspace, grown on demand by sttsv_apply_batch
   int batch_cap = 0;
   void* batch_mem = nullptr;
@@ -300,6 +306,7 @@ static void free_plan(sttsv_plan_s* p) {
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
   if (p->h_lambda) cudaFreeHost(p->h_lambda);
   if (p->batch_mem) cudaFree(p->batch_mem);
+  if (p->det_mem) cudaFree(p->det_mem);
   delete p;
 }
 
@@ -321,7 +328,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (world < 1 || rank < 0 || rank >= world) return fail(STTSV_ERR_INVALID_ARGUMENT, "bad world/rank");
   if (comm && (comm->world != world || comm->rank != rank || comm->device != device))
     return fail(STTSV_ERR_INVALID_ARGUMENT, "comm world/rank/device differ from the plan's");
-  const uint32_t known = STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES;
+  const uint32_t known = STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES | STTSV_DETERMINISTIC;
   if (flags & ~known) return fail(STTSV_ERR_UNSUPPORTED, "flags 0x%x not implemented in this build", flags & ~known);
 
   // ---- validate; offsets
@@ -550,6 +557,43 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.chunk = std::max<int64_t>(1, tiles / (grid * 16));
   if (const char* env = getenv("STTSV_CHUNK")) kp.chunk = std::max(1, atoi(env));
 
+  // ---- deterministic mode: every stored incidence gets a slot in a vertex-major
+  // buffer (vertex v's incidences in bucket / edge / member order), and each
+  // vertex's segment is cut into chunks of <= kDetChunk for the fixed-order sum
+  std::vector<int32_t> h_slot;
+  std::vector<int64_t> h_cstart, h_vchunk;
+  int64_t det_total = 0;
+  if (flags & STTSV_DETERMINISTIC) {
+    p->det = true;
+    std::vector<int64_t> voff(na + 1, 0);
+    for (int i = 0; i < kp.nb; ++i) {
+      const BucketDesc& bd = kp.b[i];
+      const int32_t* col = h_ids.data() + bd.ids_off;
+      for (int r = 0; r < bd.k; ++r)
+        for (int64_t j = 0; j < bd.m; ++j) voff[col[r * bd.stride + j] + 1]++;
+    }
+    for (int64_t v = 0; v < na; ++v) voff[v + 1] += voff[v];
+    det_total = voff[na];
+    if (det_total >= INT32_MAX) { free_plan(p); return fail(STTSV_ERR_UNSUPPORTED, "deterministic mode needs < 2^31 incidences per shard"); }
+    h_slot.assign(h_ids.size(), (int32_t)det_total);  // padding -> trash slot det_total
+    std::vector<int64_t> cur(voff.begin(), voff.end() - 1);
+    for (int i = 0; i < kp.nb; ++i) {
+      const BucketDesc& bd = kp.b[i];
+      const int32_t* col = h_ids.data() + bd.ids_off;
+      int32_t* sc = h_slot.data() + bd.ids_off;
+      for (int64_t j = 0; j < bd.m; ++j)
+        for (int r = 0; r < bd.k; ++r) sc[r * bd.stride + j] = (int32_t)cur[col[r * bd.stride + j]]++;
+    }
+    h_vchunk.resize(na + 1);
+    for (int64_t v = 0; v < na; ++v) {
+      h_vchunk[v] = (int64_t)h_cstart.size();
+      for (int64_t a = voff[v]; a < voff[v + 1]; a += kDetChunk) h_cstart.push_back(a);
+    }
+    h_vchunk[na] = (int64_t)h_cstart.size();
+    p->det_chunks = (int64_t)h_cstart.size();
+    h_cstart.push_back(det_total);
+  }
+
   // ---- device memory: one allocation
   DeviceGuard g(device);
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -584,6 +628,25 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.gs = gs;
   kp.ya = p->d_ya;
   kp.tile_counter = d_cnt;
+  if (p->det) {
+    const size_t a_slot = align(h_slot.size() * 4), a_con = align((det_total + 1) * 8),
+                 a_cs = align(h_cstart.size() * 8), a_sum = align(p->det_chunks * 8 + 8), a_vc = align(h_vchunk.size() * 8);
+    ce = cudaMalloc(&p->det_mem, a_slot + a_con + a_cs + a_sum + a_vc);
+    if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc deterministic buffers"); }
+    char* db = (char*)p->det_mem;
+    int32_t* d_slot = (int32_t*)db;
+    p->d_contrib = (double*)(db + a_slot);
+    p->d_cstart = (int64_t*)(db + a_slot + a_con);
+    p->d_csum = (double*)(db + a_slot + a_con + a_cs);
+    p->d_vchunk = (int64_t*)(db + a_slot + a_con + a_cs + a_sum);
+    ce = cudaMemcpy(d_slot, h_slot.data(), h_slot.size() * 4, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(p->d_cstart, h_cstart.data(), h_cstart.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(p->d_vchunk, h_vchunk.data(), h_vchunk.size() * 8, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "deterministic upload"); }
+    kp.slot = d_slot;
+    kp.contrib = p->d_contrib;
+    p->dbytes += a_slot + a_con + a_cs + a_sum + a_vc;
+  }
   kp.nvec = 1;
   kp.xg_vstride = (int64_t)na * gs;
   kp.ya_vstride = na;
@@ -625,6 +688,7 @@ extern "C" int sttsv_apply_launches(sttsv_plan_t p) {
   int l = 0;
   if (p->n_active > 0) l += 2;          // gather + expand
   if (p->kp.num_tiles > 0) l += 1;      // edge kernel
+  if (p->det) l += 2;                   // deterministic chunk + vertex sums
   return l;
 }
 
@@ -665,7 +729,7 @@ static sttsv_status_t check_async(sttsv_plan_s* p) {
 // y_a = (B x_a^{N-1}) on the active vertices (x_a already gathered)
 static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
   if (p->n_active == 0) return STTSV_OK;
-  CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
+  if (!p->det) CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
   if (p->kp.num_tiles > 0) {
     std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
     if (p->profiling) {
@@ -679,9 +743,12 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
       CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
     }
     CUDA_TRY(cudaMemsetAsync(p->kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
-    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s), "edge kernel launch");
+    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0), "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }
+  if (p->det)  // fixed-order sums of the vertex-major buffer (every active vertex written)
+    CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk, p->d_ya,
+                               p->n_active, s), "deterministic reduce launch");
   if (p->comm && p->world > 1) {
     NcclApi* api = nccl_api();
     ncclResult_t r = api->AllReduce(p->d_ya, p->d_ya, (size_t)p->n_active, ncclFloat64, ncclSum, p->comm->comm, s);
@@ -809,6 +876,7 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
   if (!p || !X || !Y) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
   if (nvec < 1 || nvec > STTSV_MAX_BATCH) return fail(STTSV_ERR_INVALID_ARGUMENT, "nvec must be in [1, %d]", STTSV_MAX_BATCH);
   if (ld < p->n) return fail(STTSV_ERR_INVALID_ARGUMENT, "ld < n");
+  if (p->det && nvec > 1) return fail(STTSV_ERR_UNSUPPORTED, "batched apply of a STTSV_DETERMINISTIC plan");
   const size_t span = ((size_t)(nvec - 1) * (size_t)ld + (size_t)p->n) * sizeof(double);
   if (overlap(X, span, Y, span)) return fail(STTSV_ERR_ALIAS, "X and Y overlap");
   DeviceGuard g(p->device);
@@ -847,7 +915,10 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       kp.ya_vstride = na;
       kp.priv = p->b_priv;
       CUDA_TRY(cudaMemsetAsync(kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
-      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1), "edge kernel launch");
+      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0)),
+               "edge kernel launch");
+      if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,
+                                             p->b_ya, na, s), "deterministic reduce launch");
     }
     if (p->comm && p->world > 1) {
       NcclApi* api = nccl_api();

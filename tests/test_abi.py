@@ -47,7 +47,7 @@ def test_status_strings():
     ([2], [1, 3], None, 0, 10, 0, "STTSV_ERR_INVALID_ARGUMENT"),
     ([2], [1, 3], None, 33, 10, 0, "STTSV_ERR_INVALID_ARGUMENT"),
     ([2], [1, 3], None, 4, 0, 0, "STTSV_ERR_INVALID_ARGUMENT"),
-    ([2], [1, 3], None, 4, 10, 4, "STTSV_ERR_UNSUPPORTED"),
+    ([2], [1, 3], None, 4, 10, 1 << 5, "STTSV_ERR_UNSUPPORTED"),
 ])
 def test_validation_errors(sizes, idx, w, N, n, flags, err):
     with pytest.raises(S.SttsvError) as ei:

@@ -308,3 +308,22 @@ def test_apply_batch(S, torch_cuda, name, m, n, nvec):
     y1 = plan.apply(X[1].contiguous())              # the single-vector path agrees
     assert rel(y1.cpu().numpy(), Yh[1]) < 1e-13
     plan.close()
+
+
+@pytest.mark.parametrize("name,m,n", [("tiny", None, None), ("mid", 300_000, None), ("large", 300_000, 2_000_000),
+                                      ("high-rank", 1_500, None), ("centrality", 100_000, None)])
+def test_deterministic(S, torch_cuda, name, m, n):
+    """f2 (STTSV_DETERMINISTIC): matches the oracle and is bit-reproducible run to run
+    (the default atomics path differs between runs in the last bits)."""
+    torch = torch_cuda
+    hg = W.generate(name, m=m, n=n)
+    plan = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC)
+    x = torch.from_numpy(hg.x).cuda()
+    ys = [plan.apply(x).cpu().numpy() for _ in range(4)]
+    assert rel(ys[0], oracle.sttsv(hg)) < TOL
+    for y in ys[1:]:
+        assert np.array_equal(y.view(np.int64), ys[0].view(np.int64))
+    # a second plan built from the same input gives the same bits
+    y2 = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC).apply(x).cpu().numpy()
+    assert np.array_equal(y2.view(np.int64), ys[0].view(np.int64))
+    plan.close()

@@ -85,6 +85,16 @@ def main():
         rec["batch4_ms"] = bmed
         rec["batch4_vector_incidences_per_s"] = 4 * hg.incidences / (bmed * 1e-3)
         del X, Y
+        # f2: deterministic plan (vertex-major stores + fixed-order sums)
+        dplan = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC)
+        for _ in range(3):
+            dplan.apply(x, y)
+        torch.cuda.synchronize()
+        dmed, _ = ev_time(lambda: dplan.apply(x, y), args.reps, stream)
+        rec["deterministic_ms"] = dmed
+        rec["deterministic_incidences_per_s"] = hg.incidences / (dmed * 1e-3)
+        dplan.close()
+        del dplan
         if name in ("tiny", "mid"):
             g = torch.cuda.CUDAGraph()
             s2 = torch.cuda.Stream()
