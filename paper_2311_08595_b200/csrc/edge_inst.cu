@@ -36,4 +36,12 @@ extern "C" int sttsv_debug_wait(unsigned long long out[4], int reset) {
   }
   return 0;
 }
+extern "C" int sttsv_debug_kcycles(unsigned long long out[2 * (STTSV_MAX_RANK + 1)], int reset) {
+  cudaMemcpyFromSymbol(out, sttsv::g_k_cycles, sizeof(unsigned long long) * 2 * (STTSV_MAX_RANK + 1));
+  if (reset) {
+    unsigned long long z[2 * (STTSV_MAX_RANK + 1)] = {0};
+    cudaMemcpyToSymbol(sttsv::g_k_cycles, z, sizeof(z));
+  }
+  return 0;
+}
 #endif

@@ -51,6 +51,7 @@ constexpr unsigned kFull = 0xffffffffu;
 #endif
 #if STTSV_WAITPROF
 __device__ unsigned long long g_wait_cycles[4];
+__device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per bucket k: cycles, tiles
 #endif
 
 
@@ -71,6 +72,10 @@ __device__ unsigned long long g_wait_cycles[4];
 #endif
 // ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
 // path: runtime member loop, prefix stack in shared memory (edge_big below)
+// suspend-time hint (ns) of the producer's mbarrier waits
+#ifndef STTSV_WAIT_HINT_NS
+#define STTSV_WAIT_HINT_NS 1000000
+#endif
 // L1 prefetch of the next member's table row in the large-rank path
 #ifndef STTSV_BIG_PREFETCH
 #define STTSV_BIG_PREFETCH 0
@@ -150,20 +155,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// producer-side wait: back off between polls so the spinning warp does not
-// steal issue slots from the consumers
+// producer-side wait: try_wait with a suspend-time hint, so the waiting thread
+// sleeps in hardware until the phase completes (or the hint expires) instead of
+// spinning and stealing issue slots from the consumers
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
   for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(STTSV_WAIT_HINT_NS)
         : "memory");
     if (ok) return;
-    __nanosleep(256);
   }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -399,9 +404,9 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
   load_series<L>(row(0), cur);  // P_0
 #pragma unroll 1
   for (int i = 1; i <= K - 3; ++i) {
+    load_series<L>(row(i), g);  // issued before the pushes: the load latency overlaps them
 #pragma unroll
     for (int j = 0; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push P_{i-1}
-    load_series<L>(row(i), g);
     prefetch_row<L>(row(i + 1));
     trunc_mul_inplace<L>(cur, g);  // P_i
   }
@@ -419,10 +424,10 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
   dep(K - 2, sid[(K - 2) * TILE], fma(w, qb, wF));
 #pragma unroll 1
   for (int i = K - 3; i >= 1; --i) {
+    load_series<L>(row(i), g);  // issued first: overlaps the pop and the coefficient below
 #pragma unroll
     for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
     dep(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF));
-    load_series<L>(row(i), g);
     if (i > 1) prefetch_row<L>(row(i - 1));
     if (i > 1) {
       trunc_mul_inplace<L>(S, g);  // S_i = g_i S_{i+1}
@@ -543,6 +548,9 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
       any = true;
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
       const int k = p.b[b].k;
+#if STTSV_WAITPROF
+      const long long kc0 = clock64();
+#endif
       const DetSink ds{DET ? p.slot + p.b[b].ids_off + (t - p.b[b].tile_begin) * TILE : nullptr, p.b[b].stride,
                        p.contrib};
       {
@@ -577,6 +585,12 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         }
       }
       __syncwarp();
+#if STTSV_WAITPROF
+      if (lane == 0) {
+        atomicAdd(&g_k_cycles[2 * k], (unsigned long long)(clock64() - kc0));
+        atomicAdd(&g_k_cycles[2 * k + 1], 1ull);
+      }
+#endif
       if (lane == 0) mbar_arrive(&empty[s]);
     }
 #if STTSV_WAITPROF

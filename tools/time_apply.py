@@ -40,6 +40,15 @@ if hasattr(lib, "sttsv_debug_wait"):
     lib.sttsv_debug_wait(buf, 1)
     print("  consumer full-barrier wait: %.1f%% of consumer cycles (%d warp samples)" % (
         100.0 * buf[0] / max(buf[1], 1), buf[2]))
+    kb = (ctypes.c_ulonglong * 66)()
+    lib.sttsv_debug_kcycles(kb, 1)
+    tot = sum(kb[2 * k] for k in range(33)) or 1
+    info = plan.info()
+    for k in range(33):
+        if kb[2 * k + 1]:
+            print("  k=%2d warp-tiles=%8d cycles share %5.1f%%  edges share %5.1f%%  cyc/warp-tile %.0f" % (
+                k, kb[2 * k + 1], 100.0 * kb[2 * k] / tot, 100.0 * info["edges_per_size"][k] / max(info["num_edges"], 1),
+                kb[2 * k] / kb[2 * k + 1]))
 print("%s lib=%s step_ms=%.4f kernel_ms=%.4f rerun_rel_diff=%.2e" % (
     name, os.path.basename(os.environ.get("STTSV_LIB_PATH", "libsttsv.so")), e0.elapsed_time(e1) / reps,
     kms / kn, err), flush=True)

@@ -16,7 +16,8 @@ N = int(sys.argv[1])
 B.build()
 out = os.path.join(ROOT, "build", "variants")
 import shutil
-shutil.rmtree(out, ignore_errors=True)  # keep the gpurun snapshot small: only this call's variants
+if not os.environ.get("VARIANTS_KEEP"):
+    shutil.rmtree(out, ignore_errors=True)  # keep the gpurun snapshot small: only this call's variants
 os.makedirs(out, exist_ok=True)
 objs = [os.path.join(B.OBJ, "edge_n%d.o" % n) for n in B.compiled_ranks() + [0] if n != N]
 objs += [os.path.join(B.OBJ, "kernels.o"), os.path.join(B.OBJ, "plan.o")]
