@@ -69,7 +69,7 @@ def test_fig1(S, torch_cuda):
     assert rel(y, [192, 108, 96, 585 / 2, 397, 169, 2393 / 7, 6]) < TIGHT
 
 
-@pytest.mark.parametrize("N", [2, 3, 5, 8, 10, 12, 16, 25, 17, 20, 32])
+@pytest.mark.parametrize("N", list(range(1, 17)) + [25, 17, 20, 24, 26, 32])
 def test_every_bucket_single_edges(S, torch_cuda, N):
     """One edge of every size k = 1..N (P13-style x_i = 1/(i+2)), each bucket's DP alone."""
     edges, xs = [], []
@@ -327,3 +327,57 @@ def test_deterministic(S, torch_cuda, name, m, n):
     y2 = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC).apply(x).cpu().numpy()
     assert np.array_equal(y2.view(np.int64), ys[0].view(np.int64))
     plan.close()
+
+
+# ------------------------------------------------ scatter tiers (SURVEY.md §4 layer 2)
+def _scatter_case(rng, n, m, N, pick):
+    edges = []
+    for _ in range(m):
+        k = int(rng.integers(2, N + 1))
+        edges.append(sorted(pick(k)))
+    return to_hg(n, N, edges, rng.uniform(0.5, 1.5, m), rng.uniform(0.05, 1.0, n))
+
+
+@pytest.mark.parametrize("N", [5, 8, 12, 25])
+def test_scatter_all_hot(S, torch_cuda, N):
+    """Every edge contains vertices 0..2 and otherwise draws from 8 hot vertices: all slots
+    are dominated by a handful of ids (long runs, mass flushes at tile boundaries)."""
+    rng = np.random.default_rng(N)
+    n = 12
+
+    def pick(k):
+        rest = rng.choice(np.arange(3, n), size=max(0, min(k, n) - 3), replace=False).tolist()
+        return [0, 1, 2] + rest
+    hg = _scatter_case(rng, n, 40_000 if N < 20 else 3_000, min(N, n) if N < 20 else 6, pick)
+    hg.rank = N
+    y, _ = gpu_apply(S, torch_cuda, hg)
+    assert rel(y, oracle.sttsv(hg)) < TOL
+
+
+@pytest.mark.parametrize("N", [5, 8, 12])
+def test_scatter_all_cold(S, torch_cuda, N):
+    """Vertices of degree ~1 over a large id range: most ids above the hot range H = 4096,
+    so contributions go straight to y_a (cold tier)."""
+    rng = np.random.default_rng(10 + N)
+    n = 200_000
+    hg = _scatter_case(rng, n, 30_000, N, lambda k: rng.choice(n, size=k, replace=False).tolist())
+    y, plan = gpu_apply(S, torch_cuda, hg)
+    assert plan.info()["n_active"] > 4096
+    assert rel(y, oracle.sttsv(hg)) < TOL
+
+
+@pytest.mark.parametrize("N", [6, 8, 25])
+def test_scatter_adversarial_runs(S, torch_cuda, N):
+    """Alternating blocks of identical edges and single distinct edges: runs that end at every
+    lane boundary and at tile boundaries, duplicated across warps and CTAs."""
+    rng = np.random.default_rng(20 + N)
+    n = 64
+    edges = []
+    for blk in range(3000 if N < 20 else 400):
+        k = int(rng.integers(2, min(N, 10 if N < 20 else 6) + 1))   # the oracle's cost grows as C(N-1, k-1)
+        e = sorted(rng.choice(n, size=k, replace=False).tolist())
+        edges += [e] * int(rng.integers(1, 40)) if blk % 2 == 0 else [e]
+    hg = to_hg(n, N, edges, rng.uniform(0.5, 1.5, len(edges)), rng.uniform(0.05, 1.0, n))
+    for flags in (0, S.STTSV_MERGE_DUPLICATES, S.STTSV_DETERMINISTIC):
+        y, _ = gpu_apply(S, torch_cuda, hg, flags=flags)
+        assert rel(y, oracle.sttsv(hg)) < TOL, flags
