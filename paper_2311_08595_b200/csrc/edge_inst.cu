@@ -23,6 +23,7 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.run_slots = EdgeCfg<STTSV_INST_N>::RMAX;
   e.big = EdgeCfg<STTSV_INST_N>::BIG ? (STTSV_BIG_LOCAL ? 2 : 1) : 0;
   e.consumers = 32 * EdgeCfg<STTSV_INST_N>::NCW;
+  e.epl = EdgeCfg<STTSV_INST_N>::EPL;
   return e;
 }
 }  // namespace sttsv

@@ -70,6 +70,7 @@ struct EdgeKernelEntry {
   int run_slots;       // slots with a register run accumulator (EdgeCfg::RMAX)
   int big;             // large-rank path (runtime member loop): 1 prefix stack in shared memory, 2 in local memory
   int consumers;       // consumer threads per CTA
+  int epl;             // consecutive edges per lane per tile (lane l: columns l*epl .. l*epl+epl-1 of its warp block)
 };
 #define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry_##n();
 STTSV_COMPILED_RANKS(STTSV_DECLARE_ENTRY)

@@ -186,12 +186,23 @@ __global__ void __launch_bounds__(kDetBlock) det_chunk_kernel(const double* __re
   }
 }
 
-__global__ void det_vertex_kernel(const double* __restrict__ csum, const int64_t* __restrict__ vchunk,
-                                  double* __restrict__ ya, int64_t n_active) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_active;
-       v += (int64_t)gridDim.x * blockDim.x) {
+// one CTA per vertex: thread j sums chunks j, j+256, ... in order, then the same
+// fixed tree as det_chunk_kernel (a hot vertex has ~1e4 chunks)
+__global__ void __launch_bounds__(kDetBlock) det_vertex_kernel(const double* __restrict__ csum,
+                                                               const int64_t* __restrict__ vchunk,
+                                                               double* __restrict__ ya) {
+  __shared__ double red[kDetBlock / 32];
+  const int64_t v = blockIdx.x;
+  const int64_t a = vchunk[v], b = vchunk[v + 1];
+  double s = 0.0;
+  for (int64_t c = a + threadIdx.x; c < b; c += kDetBlock) s += csum[c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int64_t c = vchunk[v]; c < vchunk[v + 1]; ++c) t += csum[c];
+    for (int w = 0; w < kDetBlock / 32; ++w) t += red[w];
     ya[v] = t;
   }
 }
@@ -264,7 +275,7 @@ cudaError_t launch_lambda(const double* z, const double* x, double* partial, dou
 cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int64_t nchunks, double* csum,
                               const int64_t* vchunk, double* ya, int64_t n_active, cudaStream_t s) {
   if (nchunks > 0) det_chunk_kernel<<<(unsigned)nchunks, kDetBlock, 0, s>>>(contrib, cstart, csum);
-  if (n_active > 0) det_vertex_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(csum, vchunk, ya, n_active);
+  if (n_active > 0) det_vertex_kernel<<<(unsigned)n_active, kDetBlock, 0, s>>>(csum, vchunk, ya);
   return cudaGetLastError();
 }
 

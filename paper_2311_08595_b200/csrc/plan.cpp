@@ -576,13 +576,23 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     det_total = voff[na];
     if (det_total >= INT32_MAX) { free_plan(p); return fail(STTSV_ERR_UNSUPPORTED, "deterministic mode needs < 2^31 incidences per shard"); }
     h_slot.assign(h_ids.size(), (int32_t)det_total);  // padding -> trash slot det_total
+    // order of a vertex's incidences = the order the kernel issues their stores:
+    // tile, warp block, step r, lane (lane l of a warp block owns columns
+    // l*epl .. l*epl+epl-1), so one warp-wide store of a hot vertex's
+    // contributions hits consecutive slots
     std::vector<int64_t> cur(voff.begin(), voff.end() - 1);
+    const int epl = p->ent.epl, wblock = 32 * epl;
     for (int i = 0; i < kp.nb; ++i) {
       const BucketDesc& bd = kp.b[i];
       const int32_t* col = h_ids.data() + bd.ids_off;
       int32_t* sc = h_slot.data() + bd.ids_off;
-      for (int64_t j = 0; j < bd.m; ++j)
-        for (int r = 0; r < bd.k; ++r) sc[r * bd.stride + j] = (int32_t)cur[col[r * bd.stride + j]]++;
+      for (int64_t wb = 0; wb * wblock < bd.m; ++wb)
+        for (int r = 0; r < epl; ++r)
+          for (int l = 0; l < 32; ++l) {
+            const int64_t j = wb * wblock + (int64_t)l * epl + r;
+            if (j >= bd.m) continue;
+            for (int q = 0; q < bd.k; ++q) sc[q * bd.stride + j] = (int32_t)cur[col[q * bd.stride + j]]++;
+          }
     }
     h_vchunk.resize(na + 1);
     for (int64_t v = 0; v < na; ++v) {
