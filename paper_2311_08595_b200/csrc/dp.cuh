@@ -25,11 +25,6 @@
 
 namespace sttsv {
 
-__device__ __forceinline__ constexpr double inv_fact_c(int j) {
-  double f = 1.0;
-  for (int i = 2; i <= j; ++i) f *= double(i);
-  return 1.0 / f;
-}
 
 // g[j] = x^{j+1}/(j+1)!, j = 0..GS-1 (the table writer)
 __device__ __forceinline__ void series_row(double x, double* __restrict__ g, int GS) {

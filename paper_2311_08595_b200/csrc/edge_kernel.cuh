@@ -3,35 +3,39 @@
 // Work decomposition.  The plan stores each cardinality bucket k as SoA int32
 // id columns + fp64 weights w' = w (N-1)!/|beta(k)| (PAPER.md:342 footnote and
 // Alg. 2's factor), edges sorted lexicographically by their
-// (degree-relabelled, ascending) member ids.  A tile is TILE = 32*NCW*EPL
-// consecutive edges of one bucket.  One persistent CTA per SM; its producer
-// grabs CHUNKS of p.chunk consecutive tiles from a global atomic counter (dynamic
-// load balance; tiles ordered most expensive bucket first, so the tail is the
-// cheapest work), so consecutive tiles of a CTA are mostly neighbours in the
-// sort order.
+// (degree-relabelled, ascending) member ids and padded to whole tiles.  A tile
+// is TILE = 32*NCW*EPL consecutive edges of one bucket.  Persistent CTAs (one or
+// two per SM); each CTA's producer grabs CHUNKS of p.chunk consecutive tiles
+// from a device counter (dynamic load balance; tiles are ordered most expensive
+// bucket first, so the tail is the cheapest work), so consecutive tiles of a
+// CTA are mostly neighbours in the sort order.
 //
 // Warp specialisation.  Per CTA, one producer warp streams tiles into an
 // STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk ->
-// SASS UBLKCP, completion on a `full` mbarrier with expect_tx); NCW consumer
-// warps each take a block of 32*EPL edges of the tile, lane l the EPL
-// CONSECUTIVE edges l*EPL .. l*EPL+EPL-1 (EPL odd: the strided shared-memory
-// reads are bank-conflict free), run the fully unrolled register DP of dp.cuh
-// for (k, L = N-k+1), and release the stage on an `empty` mbarrier.  No
-// CTA-wide barrier sits on the tile loop; bucket dispatch is once per tile.
+// SASS UBLKCP, completion on a `full` mbarrier with expect_tx) and publishes the
+// tile index in the stage; NCW consumer warps each take a block of 32*EPL edges
+// of the tile, lane l the EPL CONSECUTIVE edges l*EPL .. l*EPL+EPL-1 (EPL odd:
+// the strided shared-memory reads are bank-conflict free), run the per-edge DP
+// of dp.cuh for (k, L = N-k+1) — fully unrolled in registers for N <= 12, a
+// runtime member loop with a local-memory prefix stack (edge_big) otherwise —
+// and release the stage on an `empty` mbarrier.  No CTA-wide barrier sits on
+// the tile loop; bucket dispatch is once per tile.
 //
 // Scatter (row a5).  Contribution d_i = w' c_i goes to vertex id[i] of slot i.
 // Because edges are sorted and a lane walks consecutive edges, it sees long
 // runs of the same vertex in each slot.  Per slot i < RMAX a lane keeps a
 // register run accumulator (rid[i], run[i]): the same vertex again is one DADD;
-// a different vertex flushes the run.  Flushes inside a tile are per lane (few
-// lanes, distinct vertices); at a tile's first step many lanes can end a run
-// of the same long-run vertex at once.  A flush is ONE predicated, fire-and-
-// forget red.global.add.f64 (SASS REDG.E.ADD.F64; the warp does not wait):
-// for v < H (hot, degree-relabelled ids) into this CTA's private slice
-// priv[cta][v] (L2-resident, contention only inside the CTA), else straight
-// into y_a.  Each CTA adds its slice into y_a once at the end.  (Shared-memory
-// fp64 atomicAdd is a CAS loop on sm_100a — ATOMS.CAST.SPIN.64 — whose latency
-// stalled the warps; there is no native shared fp64 red.)
+// a different vertex flushes the run with ONE fire-and-forget
+// red.global.add.f64 (SASS REDG.E.ADD.F64; the warp does not wait): for v < H
+// (hot, degree-relabelled ids) into this CTA's private slice priv[cta][v]
+// (L2-resident, contention only inside the CTA), else straight into y_a.  Each
+// CTA adds its slice into y_a once at the end.  (Shared-memory fp64 atomicAdd
+// is a CAS loop on sm_100a — ATOMS.CAST.SPIN.64 — whose latency stalled the
+// warps; there is no native shared fp64 red.)
+//
+// Variants (template flags): BATCH — nvec vectors per staged tile (f4,
+// sttsv_apply_batch); DET — each contribution is stored to its plan-time slot
+// of a vertex-major buffer instead (f2, STTSV_DETERMINISTIC).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -55,12 +59,14 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #endif
 
 
+// ---- compile-time tuning (each default was chosen by A/B timing on B200 with
+// tools/variants.py + tools/time_apply.py)
+// small ranks (N <= 10): two CTAs per SM, each 7 consumer warps + 1 producer
+// with a 110 KB ring (two independent TMA pipelines per SM measured 2.7% faster
+// than one CTA of 15 consumers on `large`), 5 edges per lane per tile
 #ifndef STTSV_EPL
 #define STTSV_EPL 5
 #endif
-// small ranks (N <= 10): two CTAs per SM, each 7 consumer warps + 1 producer
-// with a 110 KB ring (two independent TMA pipelines per SM measured 2.7% faster
-// than one CTA of 15 consumers on `large`)
 #ifndef STTSV_RING_KB
 #define STTSV_RING_KB 110
 #endif
@@ -70,34 +76,27 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #ifndef STTSV_MIN_BLOCKS
 #define STTSV_MIN_BLOCKS 2
 #endif
-// ranks >= STTSV_BIG_MIN (and the generic N = 0 kernel) use the large-rank
-// path: runtime member loop, prefix stack in shared memory (edge_big below)
-// suspend-time hint (ns) of the producer's mbarrier waits
-#ifndef STTSV_WAIT_HINT_NS
-#define STTSV_WAIT_HINT_NS 1000000
-#endif
-// L1 prefetch of the next member's table row in the large-rank path
-#ifndef STTSV_BIG_PREFETCH
-#define STTSV_BIG_PREFETCH 0
-#endif
-// CTAs per SM of the unrolled kernel for N = 11..(BIG_MIN-1)
+// N = 11 .. BIG_MIN-1: one CTA per SM with 11 consumer warps (168 registers, no spills)
 #ifndef STTSV_MID_BLOCKS
 #define STTSV_MID_BLOCKS 1
 #endif
-// consumer warps of the unrolled kernel for N = 11..(BIG_MIN-1)
 #ifndef STTSV_NCW_MID
 #define STTSV_NCW_MID 11
 #endif
+// N >= BIG_MIN and the generic runtime-N kernel (N = 0): large-rank path with the
+// prefix stack in L1-cached local memory (BIG_LOCAL = 1) or shared memory (0)
 #ifndef STTSV_BIG_MIN
 #define STTSV_BIG_MIN 13
 #endif
-// 1: the large-rank prefix stack is a per-thread local-memory array (L1-cached)
-// instead of shared memory, which allows more consumer warps
 #ifndef STTSV_BIG_LOCAL
 #define STTSV_BIG_LOCAL 1
 #endif
 #ifndef STTSV_BIG_NCW
 #define STTSV_BIG_NCW 11
+#endif
+// suspend-time hint (ns) of the producer's mbarrier waits
+#ifndef STTSV_WAIT_HINT_NS
+#define STTSV_WAIT_HINT_NS 1000000
 #endif
 
 template <int N>
@@ -110,9 +109,8 @@ struct EdgeCfg {
   // path also needs its prefix stack)
   static constexpr int RING_BUDGET =
       BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024 : (N <= 10 ? STTSV_RING_KB : 220 / STTSV_MID_BLOCKS) * 1024;
-  // consumer warps: 15 (+1 producer = 4 warps per SMSP) for small ranks; fewer
-  // when two stages of the largest bucket would not fit the ring budget; the
-  // large-rank path runs 4 (2 for the generic kernel) register-heavy warps
+  // consumer warps per CTA (NCW_PREF), fewer when two stages of the largest
+  // bucket would not fit the ring budget
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
   static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 10 ? STTSV_NCW_SMALL : STTSV_NCW_MID);
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
@@ -183,10 +181,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// L2 prefetch of a global range (no shared memory, no completion tracking)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 
 // ------------------------------------------------------------ scatter
 struct Sink {
@@ -321,18 +315,11 @@ __device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const dou
 // For large L = N-K+1 a lane cannot hold K series in registers.  One edge per
 // lane; members are walked by a RUNTIME loop; the working rows (current prefix
 // P, one member row g, suffix S) are L-long register arrays; the prefix stack
-// P_0..P_{K-4} lives in shared memory (thread-interleaved: conflict-free), and
-// each member's series row is (re)loaded from the L1/L2-resident table where
-// it is used.  Products are formed in place (descending coefficient order).
+// P_0..P_{K-4} lives in per-thread local memory (STTSV_BIG_LOCAL = 1, L1-cached)
+// or thread-interleaved shared memory; each member's series row is loaded from
+// the L1/L2-resident table where it is used.  Products are formed in place
+// (descending coefficient order).
 
-// L1 prefetch of a table row's first L coefficients (one instruction per 128-B line)
-template <int L>
-__device__ __forceinline__ void prefetch_row(const double* row) {
-#if STTSV_BIG_PREFETCH
-#pragma unroll
-  for (int j = 0; j < L; j += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + j));
-#endif
-}
 
 // a = (a*b) mod t^L, in place
 template <int L>
@@ -400,17 +387,14 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
     return;
   }
   double cur[L], g[L], S[L];
-  prefetch_row<L>(row(1));
   load_series<L>(row(0), cur);  // P_0
 #pragma unroll 1
   for (int i = 1; i <= K - 3; ++i) {
     load_series<L>(row(i), g);  // issued before the pushes: the load latency overlaps them
 #pragma unroll
     for (int j = 0; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push P_{i-1}
-    prefetch_row<L>(row(i + 1));
     trunc_mul_inplace<L>(cur, g);  // P_i
   }
-  prefetch_row<L>(row(K - 1));
   // cur = P_{K-3}
   load_series<L>(row(K - 2), g);
   load_series<L>(row(K - 1), S);
@@ -428,7 +412,6 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
 #pragma unroll
     for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
     dep(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF));
-    if (i > 1) prefetch_row<L>(row(i - 1));
     if (i > 1) {
       trunc_mul_inplace<L>(S, g);  // S_i = g_i S_{i+1}
     } else {

@@ -98,7 +98,6 @@ cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)
 cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,
                              int N, cudaStream_t s);
-cudaError_t launch_fill_const(double* y, int64_t n, double v, cudaStream_t s);
 cudaError_t launch_lambda(const double* z, const double* x, double* partial, double* out, int64_t n_active, int N,
                           cudaStream_t s);
 

@@ -34,10 +34,6 @@ __global__ void expand_kernel(const double* __restrict__ ya, const int32_t* __re
     y[act[i]] = ya[i];
 }
 
-__global__ void fill_kernel(double* __restrict__ y, int64_t n, double v) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = v;
-}
 
 constexpr int kNormBlock = 1024;
 constexpr int kNormMaxGrid = kNormalizeScratch;
@@ -279,11 +275,6 @@ cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int6
   return cudaGetLastError();
 }
 
-cudaError_t launch_fill_const(double* y, int64_t n, double v, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  fill_kernel<<<grid_for(n, 256, 8192), 256, 0, s>>>(y, n, v);
-  return cudaGetLastError();
-}
 
 // x and z are n_active long; `partial` holds kNormalizeScratch doubles.
 cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,
