@@ -391,8 +391,10 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
 #pragma unroll 1
   for (int i = 1; i <= K - 3; ++i) {
     load_series<L>(row(i), g);  // issued before the pushes: the load latency overlaps them
+    if (i > 1) {                // P_0 = g_0 is re-read from the table later, not stacked
 #pragma unroll
-    for (int j = 0; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push P_{i-1}
+      for (int j = 0; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push P_{i-1}
+    }
     trunc_mul_inplace<L>(cur, g);  // P_i
   }
   // cur = P_{K-3}
@@ -409,8 +411,12 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
 #pragma unroll 1
   for (int i = K - 3; i >= 1; --i) {
     load_series<L>(row(i), g);  // issued first: overlaps the pop and the coefficient below
+    if (i > 1) {
 #pragma unroll
-    for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
+      for (int j = 0; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop P_{i-1}
+    } else {
+      load_series<L>(row(0), cur);  // P_0 = g_0 (the hottest row: L1-resident)
+    }
     dep(i, sid[i * TILE], fma(w, coef<D, L>(cur, S), wF));
     if (i > 1) {
       trunc_mul_inplace<L>(S, g);  // S_i = g_i S_{i+1}
