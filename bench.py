@@ -258,9 +258,13 @@ def run_ours(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
-    e2e = {"value": hg.incidences / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 8),
+    sparse_x = info["n_active"] * 8 <= hg.n   # sttsv_apply_host copies only x on the active vertices
+    e2e = {"value": hg.incidences / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(info["n_active"] * 8 if sparse_x else xh.numel() * 8),
            "d2h_bytes_per_step": int(yh.numel() * 8), "ms_per_step": e2e_s * 1e3,
-           "timing": "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
+           "timing": "host perf_counter around synchronous sttsv_apply_host (pinned buffers; x gathered on the "
+                     "host to the %d active vertices)" % info["n_active"] if sparse_x else
+                     "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
 
     # ---------------- roofline of the dominant kernel (edge kernel)
     alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]

@@ -138,9 +138,11 @@ sttsv_status_t sttsv_apply(sttsv_plan_t plan, const double* x_dev, double* y_dev
 sttsv_status_t sttsv_apply_batch(sttsv_plan_t plan, const double* X_dev, double* Y_dev, int nvec, int64_t ld,
                                  void* stream);
 
-/* sttsv_apply_host — the same product from HOST vectors: copies x (fp64[n])
- * to the device, applies, copies y (fp64[n]) back, and synchronises before
- * returning.  Host buffers may be pageable; pinned buffers are faster. */
+/* sttsv_apply_host — the same product from HOST vectors, synchronous.  When the
+ * active set is sparse (n_active <= n/8) only x on the active vertices crosses
+ * PCIe (gathered on the host into a pinned buffer); otherwise all of x (fp64[n])
+ * is copied.  y (fp64[n]) is copied back in full.  Host buffers may be
+ * pageable; a pinned y is faster. */
 sttsv_status_t sttsv_apply_host(sttsv_plan_t plan, const double* x_host, double* y_host);
 
 /* sttsv_power_iterate — the x-update of Alg. 1 (NQZ, PAPER.md:351-355 lines 3-6),

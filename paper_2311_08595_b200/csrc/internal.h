@@ -94,6 +94,7 @@ cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int6
 constexpr int kDetChunk = 4096;  // contributions per deterministic reduction chunk
 cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
                           cudaStream_t s);
+cudaError_t launch_series(const double* xa, double* xg, int gs, int64_t n_active, cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)
 cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,

@@ -27,6 +27,13 @@ __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __res
   }
 }
 
+// series table rows from x_a (sttsv_apply_host's host-gathered path)
+__global__ void series_kernel(const double* __restrict__ xa, double* __restrict__ xg, int gs, int64_t n_active) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
+       i += (int64_t)gridDim.x * blockDim.x)
+    series_row(xa[i], xg + i * gs, gs);
+}
+
 __global__ void expand_kernel(const double* __restrict__ ya, const int32_t* __restrict__ act,
                               double* __restrict__ y, int64_t n_active) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
@@ -250,6 +257,12 @@ cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, doubl
                           cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
   gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_series(const double* xa, double* xg, int gs, int64_t n_active, cudaStream_t s) {
+  if (n_active <= 0) return cudaSuccess;
+  series_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(xa, xg, gs, n_active);
   return cudaGetLastError();
 }
 

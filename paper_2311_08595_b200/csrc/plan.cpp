@@ -224,6 +224,8 @@ struct sttsv_plan_s {
   double* d_yhost = nullptr;
   cudaStream_t host_stream = nullptr;
   double* h_lambda = nullptr;  // pinned (lambda_min, lambda_max) of sttsv_hec
+  std::vector<int32_t> h_act;  // host copy of act[] (sttsv_apply_host gathers x on the host)
+  double* h_xa = nullptr;      // pinned staging of x on the active vertices
   // deterministic mode (STTSV_DETERMINISTIC): slot pool, vertex-major buffer, chunks
   bool det = false;
   void* det_mem = nullptr;
@@ -305,6 +307,7 @@ static void free_plan(sttsv_plan_s* p) {
   if (p->d_xhost) cudaFree(p->d_xhost);
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
   if (p->h_lambda) cudaFreeHost(p->h_lambda);
+  if (p->h_xa) cudaFreeHost(p->h_xa);
   if (p->batch_mem) cudaFree(p->batch_mem);
   if (p->det_mem) cudaFree(p->det_mem);
   delete p;
@@ -630,6 +633,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
+  p->h_act = act;
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
   kp.ids = d_ids;
   kp.w = d_w;
@@ -800,9 +804,29 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
     p->d_yhost = p->d_xhost + p->n;
   }
   cudaStream_t s = p->host_stream;
-  CUDA_TRY(cudaMemcpyAsync(p->d_xhost, x_host, bytes, cudaMemcpyHostToDevice, s), "H2D x");
-  sttsv_status_t st = sttsv_apply(p, p->d_xhost, p->d_yhost, s);
-  if (st != STTSV_OK) return st;
+  const int64_t na = p->n_active;
+  if (na > 0 && na * 8 <= p->n) {
+    // sparse active set: only x on the active vertices crosses PCIe.  Gather it
+    // on the host (OpenMP) into a pinned buffer, copy n_a doubles, build the
+    // series table from it, apply, expand, copy y back.
+    if (!p->h_xa) CUDA_TRY(cudaMallocHost(&p->h_xa, (size_t)na * sizeof(double)), "cudaMallocHost x_a");
+    const int32_t* act = p->h_act.data();
+    double* xa = p->h_xa;
+#pragma omp parallel for schedule(static) if (na > 16384)
+    for (int64_t i = 0; i < na; ++i) xa[i] = x_host[act[i]];
+    sttsv_status_t st0 = check_async(p);
+    if (st0 != STTSV_OK) return st0;
+    CUDA_TRY(cudaMemcpyAsync(p->d_xa, p->h_xa, (size_t)na * sizeof(double), cudaMemcpyHostToDevice, s), "H2D x_a");
+    CUDA_TRY(launch_series(p->d_xa, p->d_xg, p->gs, na, s), "series launch");
+    sttsv_status_t st = apply_active(p, s);
+    if (st != STTSV_OK) return st;
+    CUDA_TRY(cudaMemsetAsync(p->d_yhost, 0, bytes, s), "memset y");
+    CUDA_TRY(launch_expand(p->d_ya, p->d_act, p->d_yhost, na, s), "expand launch");
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(p->d_xhost, x_host, bytes, cudaMemcpyHostToDevice, s), "H2D x");
+    sttsv_status_t st = sttsv_apply(p, p->d_xhost, p->d_yhost, s);
+    if (st != STTSV_OK) return st;
+  }
   CUDA_TRY(cudaMemcpyAsync(y_host, p->d_yhost, bytes, cudaMemcpyDeviceToHost, s), "D2H y");
   CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
   return STTSV_OK;

@@ -218,12 +218,18 @@ def test_nccl_world1(S, torch_cuda):
         S.sttsv_comm_destroy(comm)
 
 
-def test_apply_host_matches_device(S, torch_cuda):
-    hg = W.generate("large", m=100_000, n=1_000_000)
+@pytest.mark.parametrize("name,m,n", [("large", 100_000, 1_000_000), ("tiny", None, None)])
+def test_apply_host_matches_device(S, torch_cuda, name, m, n):
+    """Host-buffer call: the sparse-active-set path (x gathered on the host, large) and the
+    dense path (tiny: every vertex active)."""
+    hg = W.generate(name, m=m, n=n)
     y, plan = gpu_apply(S, torch_cuda, hg)
-    yh = plan.apply_host(hg.x)
-    assert rel(yh, y) < 1e-14
+    for _ in range(2):
+        yh = plan.apply_host(hg.x)
+        assert rel(yh, y) < 1e-14
     assert rel(yh, oracle.sttsv(hg)) < TOL
+    x2 = np.random.default_rng(1).uniform(0.1, 1.0, hg.n)     # a second x through the same staging
+    assert rel(plan.apply_host(x2), oracle.sttsv(hg, x=x2)) < TOL
 
 
 # ------------------------------------------- full BASELINE sizes (bench launch config)
