@@ -387,3 +387,35 @@ def test_scatter_adversarial_runs(S, torch_cuda, N):
     for flags in (0, S.STTSV_MERGE_DUPLICATES, S.STTSV_DETERMINISTIC):
         y, _ = gpu_apply(S, torch_cuda, hg, flags=flags)
         assert rel(y, oracle.sttsv(hg)) < TOL, flags
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_fuzz(S, torch_cuda, seed):
+    """Random ranks (compiled and generic kernels), sizes, duplicates, flags and entry points."""
+    torch = torch_cuda
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.integers(1, 33))
+    n = int(rng.integers(2, 3000))
+    m = int(rng.integers(1, 2500))
+    kmax = min(N, n, 12 if N <= 16 else 5)          # the oracle enumerates C(N-1, k-1) multisets per edge
+    edges = [sorted(rng.choice(n, size=int(rng.integers(1, kmax + 1)), replace=False).tolist()) for _ in range(m)]
+    if seed % 3 == 0:                                  # heavy duplication
+        edges = edges[: max(1, m // 10)] * 10
+    hg = to_hg(n, N, edges, rng.uniform(0.1, 2.0, len(edges)), rng.uniform(0.01, 1.0, n))
+    flags = [0, S.STTSV_MERGE_DUPLICATES, S.STTSV_DETERMINISTIC][seed % 3]
+    plan = S.Plan.from_hypergraph(hg, flags=flags)
+    ref = oracle.sttsv(hg)
+    mode = seed % 4
+    if mode == 0:
+        y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
+    elif mode == 1:
+        y = plan.apply_host(hg.x)
+    elif mode == 2 and flags != S.STTSV_DETERMINISTIC:
+        X = torch.from_numpy(np.stack([hg.x, 0.5 * hg.x])).cuda()
+        Y = plan.apply_batch(X).cpu().numpy()
+        assert rel(Y[1], 0.5 ** (N - 1) * ref) < TOL     # homogeneity
+        y = Y[0]
+    else:
+        y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
+    assert rel(y, ref) < TOL, (seed, N, n, m, flags, mode)
+    plan.close()
