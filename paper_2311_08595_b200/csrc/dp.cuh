@@ -26,14 +26,26 @@
 namespace sttsv {
 
 
-// g[j] = x^{j+1}/(j+1)!, j = 0..GS-1 (the table writer)
-__device__ __forceinline__ void series_row(double x, double* __restrict__ g, int GS) {
-  double pw = x, f = 1.0;
-  g[0] = pw;
-  for (int j = 1; j < GS; ++j) {
-    pw *= x;
-    f *= double(j + 1);
-    g[j] = pw * (1.0 / f);
+// The table writer.  norm = 0: g[j] = x^{j+1}/(j+1)!, j = 0..GS-1.
+// norm = 1 (large-rank path): g[0] = x and g[j] = h[j] = x^j/(j+1)! for j >= 1,
+// the series normalised to a leading 1 (g_full = x * h, h[0] = 1 implicit).
+__device__ __forceinline__ void series_row(double x, double* __restrict__ g, int GS, int norm = 0) {
+  if (norm) {
+    double pw = 1.0, f = 1.0;
+    g[0] = x;
+    for (int j = 1; j < GS; ++j) {
+      pw *= x;
+      f *= double(j + 1);
+      g[j] = pw * (1.0 / f);
+    }
+  } else {
+    double pw = x, f = 1.0;
+    g[0] = pw;
+    for (int j = 1; j < GS; ++j) {
+      pw *= x;
+      f *= double(j + 1);
+      g[j] = pw * (1.0 / f);
+    }
   }
 }
 

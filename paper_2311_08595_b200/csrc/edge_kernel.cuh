@@ -94,6 +94,10 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #ifndef STTSV_BIG_NCW
 #define STTSV_BIG_NCW 11
 #endif
+// large-rank path on series normalised to a leading 1 (fewer FP64 operations)
+#ifndef STTSV_BIG_NORM
+#define STTSV_BIG_NORM 1
+#endif
 // suspend-time hint (ns) of the producer's mbarrier waits
 #ifndef STTSV_WAIT_HINT_NS
 #define STTSV_WAIT_HINT_NS 1000000
@@ -427,13 +431,136 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
   if (K == 3) dep(0, sid[0], fma(w, S[D], wF));  // S = S_1
 }
 
+// ---- normalised variant (STTSV_BIG_NORM): table rows hold x in slot 0 and
+// h[j] = x^j/(j+1)! (h[0] = 1 implicit), so g_u = x_u h_u.  Products of
+// normalised series keep a leading 1: a truncated product costs L(L-1)/2
+// operations instead of L(L+1)/2, and the scalar factors prod x_u are carried
+// separately (prefix product X on the stack row's slot 0, suffix product Xs).
+// Every term is still a product of positive numbers for x > 0.
+
+// a = (a*b) mod t^L for a[0] = b[0] = 1 (slot 0 untouched), in place
+template <int L>
+__device__ __forceinline__ void trunc_mul_norm_inplace(double (&a)[L], const double (&b)[L]) {
+#pragma unroll
+  for (int j = L - 1; j >= 1; --j) {
+    double s = a[j] + b[j];
+#pragma unroll
+    for (int i = 1; i < j; ++i) s = fma(a[i], b[j - i], s);
+    a[j] = s;
+  }
+}
+
+// [t^D] (a*b) for a[0] = b[0] = 1
+template <int D, int L>
+__device__ __forceinline__ double coef_norm(const double (&a)[L], const double (&b)[L]) {
+  static_assert(D < L, "coef degree");
+  if constexpr (D == 0) {
+    return 1.0;
+  } else {
+    double s = a[D] + b[D];
+#pragma unroll
+    for (int j = 1; j < D; ++j) s = fma(a[j], b[D - j], s);
+    return s;
+  }
+}
+
+// load a normalised row: returns x, fills h[0] = 1, h[1..L-1]
+template <int L>
+__device__ __forceinline__ double load_norm(const double* __restrict__ row, double (&h)[L]) {
+  load_series<L>(row, h);
+  const double x = h[0];
+  h[0] = 1.0;
+  return x;
+}
+
+template <int L, int TILE, int NT, int RB, bool DET>
+__device__ __forceinline__ void edge_big_norm(int K, const int32_t* __restrict__ sid, double w,
+                                              const double* __restrict__ xg, int gs, double* __restrict__ stk,
+                                              RunAcc<RB>& ra, const Sink& sk, const DetSink& ds, int col) {
+  constexpr int D = L - 1;
+  auto row = [&](int i) { return xg + (size_t)(uint32_t)sid[i * TILE] * gs; };
+  auto dep = [&](int i, int v, double d) {
+    if constexpr (DET) ds.contrib[__ldg(ds.slot + i * ds.sstride + col)] = d;
+    else dep_slot<RB>(i, v, d, ra, sk);
+  };
+  if (K == 1) {
+    // singleton: q = [D == 0], F = g_0[D-1] = x h[D-1]
+    const double* r = row(0);
+    const double x = __ldg(r);
+    const double F = D >= 1 ? (D == 1 ? x : x * __ldg(r + (D >= 2 ? D - 1 : 0))) : 0.0;
+    dep(0, sid[0], w * ((D == 0 ? 1.0 : 0.0) + F));
+    return;
+  }
+  if (K == 2) {
+    double a[L], b[L];
+    const double xa = load_norm<L>(row(0), a);
+    const double xb = load_norm<L>(row(1), b);
+    double F = 0.0;
+    if constexpr (D >= 1) F = xa * xb * coef_norm<D - 1, L>(a, b);
+    const double wF = w * F;
+    dep(0, sid[0], fma(w, xb * b[D], wF));   // g_1[D] = x_1 h_1[D]
+    dep(1, sid[TILE], fma(w, xa * a[D], wF));
+    return;
+  }
+  double cur[L], g[L], S[L];
+  double X = load_norm<L>(row(0), cur);  // P_0 = h_0, scalar prefix x_0
+#pragma unroll 1
+  for (int i = 1; i <= K - 3; ++i) {
+    const double xi = load_norm<L>(row(i), g);
+    if (i > 1) {  // P_0 = h_0 is re-read from the table later, not stacked
+      stk[((i - 1) * L) * NT] = X;
+#pragma unroll
+      for (int j = 1; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];  // push (X_{i-1}, P_{i-1})
+    }
+    trunc_mul_norm_inplace<L>(cur, g);  // P_i
+    X *= xi;
+  }
+  // cur = P_{K-3} (normalised), X = x_0 ... x_{K-3}
+  const double xa = load_norm<L>(row(K - 2), g);
+  const double xb = load_norm<L>(row(K - 1), S);
+  const double qa = X * xa * coef_norm<D, L>(cur, g);  // [t^D] P_{K-2}          -> member K-1
+  const double qb = X * xb * coef_norm<D, L>(cur, S);  // [t^D] P_{K-3} g_{K-1}  -> member K-2
+  trunc_mul_norm_inplace<L>(S, g);                     // S_{K-2} (normalised)
+  double Xs = xa * xb;
+  double F = 0.0;
+  if constexpr (D >= 1) F = X * Xs * coef_norm<D - 1, L>(cur, S);
+  const double wF = w * F;
+  dep(K - 1, sid[(K - 1) * TILE], fma(w, qa, wF));
+  dep(K - 2, sid[(K - 2) * TILE], fma(w, qb, wF));
+#pragma unroll 1
+  for (int i = K - 3; i >= 1; --i) {
+    const double xi = load_norm<L>(row(i), g);
+    double Xp;
+    if (i > 1) {
+      Xp = stk[((i - 1) * L) * NT];
+#pragma unroll
+      for (int j = 1; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop (X_{i-1}, P_{i-1})
+      cur[0] = 1.0;
+    } else {
+      Xp = load_norm<L>(row(0), cur);  // P_0 = h_0 (the hottest row: L1-resident)
+    }
+    dep(i, sid[i * TILE], fma(w, Xp * Xs * coef_norm<D, L>(cur, S), wF));
+    if (i > 1) {
+      trunc_mul_norm_inplace<L>(S, g);  // S_i = g_i S_{i+1}
+      Xs *= xi;
+    } else {
+      dep(0, sid[0], fma(w, xi * Xs * coef_norm<D, L>(g, S), wF));  // [t^D] g_1 S_2
+    }
+  }
+  if (K == 3) dep(0, sid[0], fma(w, Xs * S[D], wF));  // S_1 = x_1 x_2 (h_1 h_2)
+}
+
 template <int L, int LMAX, int TILE, int NT, int RB, bool DET>
 __device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid, double w, const double* xg, int gs,
                                              double* stk, RunAcc<RB>& ra, const Sink& sk, const DetSink& ds,
                                              int col) {
   if constexpr (L <= LMAX) {
     if (L_rt == L) {
+#if STTSV_BIG_NORM
+      edge_big_norm<L, TILE, NT, RB, DET>(K, sid, w, xg, gs, stk, ra, sk, ds, col);
+#else
       edge_big<L, TILE, NT, RB, DET>(K, sid, w, xg, gs, stk, ra, sk, ds, col);
+#endif
       return;
     }
     dispatch_big<L + 1, LMAX, TILE, NT, RB, DET>(L_rt, K, sid, w, xg, gs, stk, ra, sk, ds, col);

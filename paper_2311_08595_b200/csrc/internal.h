@@ -70,6 +70,7 @@ struct EdgeKernelEntry {
   int run_slots;       // slots with a register run accumulator (EdgeCfg::RMAX)
   int big;             // large-rank path (runtime member loop): 1 prefix stack in shared memory, 2 in local memory
   int consumers;       // consumer threads per CTA
+  int table_norm;      // series table rows normalised to a leading 1 (dp.cuh series_row norm = 1)
   int epl;             // consecutive edges per lane per tile (lane l: columns l*epl .. l*epl+epl-1 of its warp block)
 };
 #define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry_##n();
@@ -92,13 +93,14 @@ cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams&
 cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int64_t nchunks, double* csum,
                               const int64_t* vchunk, double* ya, int64_t n_active, cudaStream_t s);
 constexpr int kDetChunk = 4096;  // contributions per deterministic reduction chunk
-cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
-                          cudaStream_t s);
-cudaError_t launch_series(const double* xa, double* xg, int gs, int64_t n_active, cudaStream_t s);
+// norm: series table format (dp.cuh series_row; EdgeKernelEntry::table_norm)
+cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
+                          int64_t n_active, cudaStream_t s);
+cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)
-cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,
-                             int N, cudaStream_t s);
+cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, int norm, double* partial,
+                             int64_t n_active, int N, cudaStream_t s);
 cudaError_t launch_lambda(const double* z, const double* x, double* partial, double* out, int64_t n_active, int N,
                           cudaStream_t s);
 

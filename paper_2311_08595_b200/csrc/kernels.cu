@@ -18,20 +18,21 @@ namespace sttsv {
 // ------------------------------------------------------- small kernels
 // x_a[i] = x[act[i]] and the series row g_i[j] = x_a[i]^{j+1}/(j+1)! (dp.cuh)
 __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __restrict__ act,
-                              double* __restrict__ xa, double* __restrict__ xg, int gs, int64_t n_active) {
+                              double* __restrict__ xa, double* __restrict__ xg, int gs, int norm, int64_t n_active) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double v = x[act[i]];
     xa[i] = v;
-    series_row(v, xg + i * gs, gs);
+    series_row(v, xg + i * gs, gs, norm);
   }
 }
 
 // series table rows from x_a (sttsv_apply_host's host-gathered path)
-__global__ void series_kernel(const double* __restrict__ xa, double* __restrict__ xg, int gs, int64_t n_active) {
+__global__ void series_kernel(const double* __restrict__ xa, double* __restrict__ xg, int gs, int norm,
+                              int64_t n_active) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
        i += (int64_t)gridDim.x * blockDim.x)
-    series_row(xa[i], xg + i * gs, gs);
+    series_row(xa[i], xg + i * gs, gs, norm);
 }
 
 __global__ void expand_kernel(const double* __restrict__ ya, const int32_t* __restrict__ act,
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kNormBlock) normalize_partial_kernel(const dou
 
 // every block sums all partials in the same order, then scales its slice
 __global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __restrict__ x,
-                                                                    double* __restrict__ xg, int gs,
+                                                                    double* __restrict__ xg, int gs, int norm,
                                                                     const double* __restrict__ partial,
                                                                     int nparts, int64_t n) {
   __shared__ double tot;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kNormBlock) normalize_apply_kernel(double* __r
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = x[i] / t;
     x[i] = v;
-    series_row(v, xg + i * gs, gs);
+    series_row(v, xg + i * gs, gs, norm);
   }
 }
 
@@ -253,16 +254,16 @@ static int grid_for(int64_t n, int block, int cap) {
   return (int)g;
 }
 
-cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int64_t n_active,
-                          cudaStream_t s) {
+cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
+                          int64_t n_active, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
-  gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, n_active);
+  gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, norm, n_active);
   return cudaGetLastError();
 }
 
-cudaError_t launch_series(const double* xa, double* xg, int gs, int64_t n_active, cudaStream_t s) {
+cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
-  series_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(xa, xg, gs, n_active);
+  series_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(xa, xg, gs, norm, n_active);
   return cudaGetLastError();
 }
 
@@ -290,12 +291,12 @@ cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int6
 
 
 // x and z are n_active long; `partial` holds kNormalizeScratch doubles.
-cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, double* partial, int64_t n_active,
-                             int N, cudaStream_t s) {
+cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, int norm, double* partial,
+                             int64_t n_active, int N, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
   const int grid = grid_for(n_active, kNormBlock, kNormMaxGrid);
   normalize_partial_kernel<<<grid, kNormBlock, 0, s>>>(z, x, partial, n_active, 1.0 / double(N - 1));
-  normalize_apply_kernel<<<grid, kNormBlock, 0, s>>>(x, xg, gs, partial, grid, n_active);
+  normalize_apply_kernel<<<grid, kNormBlock, 0, s>>>(x, xg, gs, norm, partial, grid, n_active);
   return cudaGetLastError();
 }
 

@@ -785,7 +785,7 @@ extern "C" sttsv_status_t sttsv_apply(sttsv_plan_t p, const double* x, double* y
   sttsv_status_t st = check_async(p);
   if (st != STTSV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->n_active, s), "gather launch");
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, s), "gather launch");
   st = apply_active(p, s);
   if (st != STTSV_OK) return st;
   CUDA_TRY(cudaMemsetAsync(y, 0, bytes, s), "memset y");
@@ -817,7 +817,7 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
     sttsv_status_t st0 = check_async(p);
     if (st0 != STTSV_OK) return st0;
     CUDA_TRY(cudaMemcpyAsync(p->d_xa, p->h_xa, (size_t)na * sizeof(double), cudaMemcpyHostToDevice, s), "H2D x_a");
-    CUDA_TRY(launch_series(p->d_xa, p->d_xg, p->gs, na, s), "series launch");
+    CUDA_TRY(launch_series(p->d_xa, p->d_xg, p->gs, p->ent.table_norm, na, s), "series launch");
     sttsv_status_t st = apply_active(p, s);
     if (st != STTSV_OK) return st;
     CUDA_TRY(cudaMemsetAsync(p->d_yhost, 0, bytes, s), "memset y");
@@ -843,11 +843,11 @@ extern "C" sttsv_status_t sttsv_power_iterate(sttsv_plan_t p, double* x, double*
   sttsv_status_t st = check_async(p);
   if (st != STTSV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->n_active, s), "gather launch");
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, s), "gather launch");
   for (int it = 0; it < iters; ++it) {
     st = apply_active(p, s);
     if (st != STTSV_OK) return st;
-    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_xg, p->gs, p->d_scratch, p->n_active, p->N, s), "normalize launch");
+    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->d_scratch, p->n_active, p->N, s), "normalize launch");
   }
   CUDA_TRY(cudaMemsetAsync(x, 0, bytes, s), "memset x");
   CUDA_TRY(launch_expand(p->d_xa, p->d_act, x, p->n_active, s), "expand x");
@@ -873,14 +873,14 @@ extern "C" sttsv_status_t sttsv_hec(sttsv_plan_t p, double* x, double* z, double
   if (!p->h_lambda) CUDA_TRY(cudaMallocHost(&p->h_lambda, 2 * sizeof(double)), "cudaMallocHost");
   double* d_lam = p->d_scratch + 2 * kNormalizeScratch;
   // Alg. 1: y = x0 (caller's, e.g. (1/n) 1); z = TTSV1(y)
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->n_active, s), "gather launch");
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, s), "gather launch");
   st = apply_active(p, s);
   if (st != STTSV_OK) return st;
   double lo = 0.0, hi = 0.0;
   int it = 0;
   while (it < max_iters) {
     // x = z^[1/(N-1)] / ||z^[1/(N-1)]||_1 ; z = TTSV1(x) ; lambda bracket of z ./ x^[N-1]
-    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_xg, p->gs, p->d_scratch, p->n_active, p->N, s),
+    CUDA_TRY(launch_normalize(p->d_ya, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->d_scratch, p->n_active, p->N, s),
              "normalize launch");
     st = apply_active(p, s);
     if (st != STTSV_OK) return st;
@@ -936,7 +936,7 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
   }
   for (int v = 0; v < nvec; ++v)
     CUDA_TRY(launch_gather(X + (size_t)v * ld, p->d_act, p->b_xa + (size_t)v * na, p->b_xg + (size_t)v * na * p->gs,
-                           p->gs, na, s), "gather launch");
+                           p->gs, p->ent.table_norm, na, s), "gather launch");
   if (na > 0) {
     CUDA_TRY(cudaMemsetAsync(p->b_ya, 0, (size_t)nvec * na * sizeof(double), s), "memset y_a");
     if (p->kp.num_tiles > 0) {
