@@ -141,4 +141,93 @@ __device__ __forceinline__ void dp_edge_table(const double* const (&rows)[K], do
   }
 }
 
+// ---- the same DP on series normalised to a leading 1 (table rows: slot 0 = x,
+// h[j] = x^j/(j+1)! for j >= 1; g_u = x_u h_u).  Truncated products of
+// normalised series skip the multiplications by the leading 1 (L(L-1)/2
+// operations instead of L(L+1)/2); the scalar prefix / suffix products of the
+// x_u are carried separately.  Used for ranks N >= 11 (L up to N-1).
+
+// r = (a*b) mod t^L with a[0] = b[0] = r[0] = 1
+template <int L>
+__device__ __forceinline__ void trunc_mul_norm(const double (&a)[L], const double (&b)[L], double (&r)[L]) {
+  r[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j < L; ++j) {
+    double s = a[j] + b[j];
+#pragma unroll
+    for (int i = 1; i < j; ++i) s = fma(a[i], b[j - i], s);
+    r[j] = s;
+  }
+}
+
+// [t^D] (a*b) with a[0] = b[0] = 1
+template <int D, int L>
+__device__ __forceinline__ double coef_n(const double (&a)[L], const double (&b)[L]) {
+  static_assert(D < L, "coef degree");
+  if constexpr (D == 0) {
+    return 1.0;
+  } else {
+    double s = a[D] + b[D];
+#pragma unroll
+    for (int j = 1; j < D; ++j) s = fma(a[j], b[D - j], s);
+    return s;
+  }
+}
+
+template <int K, int L>
+__device__ __forceinline__ void dp_edge_table_norm(const double* const (&rows)[K], double (&q)[K], double& F) {
+  constexpr int D = L - 1;
+  F = 0.0;
+  if constexpr (K == 1) {
+    // singleton: q = [D == 0], F = g_0[D-1] = x h[D-1]
+    const double x = __ldg(rows[0]);
+    q[0] = D == 0 ? 1.0 : 0.0;
+    if constexpr (D == 1) F = x;
+    if constexpr (D >= 2) F = x * __ldg(rows[0] + (D - 1));
+  } else {
+    double h[K][L], x[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      load_series<L>(rows[i], h[i]);
+      x[i] = h[i][0];
+      h[i][0] = 1.0;
+    }
+    if constexpr (K == 2) {
+      if constexpr (D >= 1) F = x[0] * x[1] * coef_n<D - 1, L>(h[0], h[1]);
+      q[0] = x[1] * h[1][D];
+      q[1] = x[0] * h[0][D];
+    } else {
+      double P[K - 2][L], Xp[K - 2];
+#pragma unroll
+      for (int j = 0; j < L; ++j) P[0][j] = h[0][j];
+      Xp[0] = x[0];
+#pragma unroll
+      for (int i = 1; i <= K - 3; ++i) {
+        trunc_mul_norm<L>(P[i - 1], h[i], P[i]);
+        Xp[i] = Xp[i - 1] * x[i];
+      }
+      q[K - 1] = Xp[K - 3] * x[K - 2] * coef_n<D, L>(P[K - 3], h[K - 2]);
+      q[K - 2] = Xp[K - 3] * x[K - 1] * coef_n<D, L>(P[K - 3], h[K - 1]);
+      double S[L];
+      trunc_mul_norm<L>(h[K - 2], h[K - 1], S);
+      double Xs = x[K - 2] * x[K - 1];
+      if constexpr (D >= 1) F = Xp[K - 3] * Xs * coef_n<D - 1, L>(P[K - 3], S);
+#pragma unroll
+      for (int i = K - 3; i >= 1; --i) {
+        q[i] = Xp[i - 1] * Xs * coef_n<D, L>(P[i - 1], S);
+        if (i > 1) {
+          double T[L];
+          trunc_mul_norm<L>(h[i], S, T);
+#pragma unroll
+          for (int j = 0; j < L; ++j) S[j] = T[j];
+          Xs *= x[i];
+        } else {
+          q[0] = x[1] * Xs * coef_n<D, L>(h[1], S);
+        }
+      }
+      if constexpr (K == 3) q[0] = Xs * S[D];
+    }
+  }
+}
+
 }  // namespace sttsv

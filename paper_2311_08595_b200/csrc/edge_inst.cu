@@ -24,7 +24,8 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.big = EdgeCfg<STTSV_INST_N>::BIG ? (STTSV_BIG_LOCAL ? 2 : 1) : 0;
   e.consumers = 32 * EdgeCfg<STTSV_INST_N>::NCW;
   e.epl = EdgeCfg<STTSV_INST_N>::EPL;
-  e.table_norm = (EdgeCfg<STTSV_INST_N>::BIG && STTSV_BIG_NORM) ? 1 : 0;
+  e.table_norm = ((EdgeCfg<STTSV_INST_N>::BIG && STTSV_BIG_NORM) ||
+                  (!EdgeCfg<STTSV_INST_N>::BIG && STTSV_INST_N >= 11 && STTSV_MID_NORM)) ? 1 : 0;
   return e;
 }
 }  // namespace sttsv
