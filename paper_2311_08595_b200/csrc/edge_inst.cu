@@ -25,7 +25,7 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.consumers = 32 * EdgeCfg<STTSV_INST_N>::NCW;
   e.epl = EdgeCfg<STTSV_INST_N>::EPL;
   e.table_norm = ((EdgeCfg<STTSV_INST_N>::BIG && STTSV_BIG_NORM) ||
-                  (!EdgeCfg<STTSV_INST_N>::BIG && STTSV_INST_N >= 11 && STTSV_MID_NORM)) ? 1 : 0;
+                  (!EdgeCfg<STTSV_INST_N>::BIG && STTSV_INST_N >= STTSV_NORM_MIN && STTSV_MID_NORM)) ? 1 : 0;
   return e;
 }
 }  // namespace sttsv

@@ -94,9 +94,12 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #ifndef STTSV_BIG_NCW
 #define STTSV_BIG_NCW 11
 #endif
-// unrolled kernel for N = 11..12 on series normalised to a leading 1
+// unrolled kernel for N >= NORM_MIN on series normalised to a leading 1
 #ifndef STTSV_MID_NORM
 #define STTSV_MID_NORM 1
+#endif
+#ifndef STTSV_NORM_MIN
+#define STTSV_NORM_MIN 2
 #endif
 // large-rank path on series normalised to a leading 1 (fewer FP64 operations)
 #ifndef STTSV_BIG_NORM
@@ -292,7 +295,7 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
     }
     const double w = sw[col];
     double q[K], F;
-    if constexpr (N >= 11 && STTSV_MID_NORM) dp_edge_table_norm<K, L>(rows, q, F);
+    if constexpr (N >= STTSV_NORM_MIN && STTSV_MID_NORM) dp_edge_table_norm<K, L>(rows, q, F);
     else dp_edge_table<K, L>(rows, q, F);
     const double wF = w * F;
     double dv[K];
