@@ -224,6 +224,9 @@ struct sttsv_plan_s {
   double* d_yhost = nullptr;
   cudaStream_t host_stream = nullptr;
   double* h_lambda = nullptr;  // pinned (lambda_min, lambda_max) of sttsv_hec
+  // side stream: zero-fills the dense output concurrently with the edge kernel
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<int32_t> h_act;  // host copy of act[] (sttsv_apply_host gathers x on the host)
   double* h_xa = nullptr;      // pinned staging of x on the active vertices
   // deterministic mode (STTSV_DETERMINISTIC): slot pool, vertex-major buffer, chunks
@@ -307,6 +310,9 @@ static void free_plan(sttsv_plan_s* p) {
   if (p->d_xhost) cudaFree(p->d_xhost);
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
   if (p->h_lambda) cudaFreeHost(p->h_lambda);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->h_xa) cudaFreeHost(p->h_xa);
   if (p->batch_mem) cudaFree(p->batch_mem);
   if (p->det_mem) cudaFree(p->det_mem);
@@ -777,6 +783,32 @@ static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
+// gather -> edge kernel (+ allreduce) -> expand into a dense y.  For a large y
+// the zero-fill of y (8n bytes of HBM writes) runs on a side stream, forked
+// from and joined back into `s`, so it overlaps the edge kernel.
+static sttsv_status_t apply_dense(sttsv_plan_s* p, const double* x, double* y, cudaStream_t s) {
+  const size_t bytes = (size_t)p->n * sizeof(double);
+  const bool fork = bytes >= ((size_t)8 << 20) && p->kp.num_tiles > 0;
+  if (fork) {
+    if (!p->side) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking), "side stream");
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "event");
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "event");
+    }
+    CUDA_TRY(cudaEventRecord(p->ev_fork, s), "fork record");
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0), "fork wait");
+    CUDA_TRY(cudaMemsetAsync(y, 0, bytes, p->side), "memset y");
+    CUDA_TRY(cudaEventRecord(p->ev_join, p->side), "join record");
+  }
+  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, s), "gather launch");
+  sttsv_status_t st = apply_active(p, s);
+  if (st != STTSV_OK) return st;
+  if (fork) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0), "join wait");
+  else CUDA_TRY(cudaMemsetAsync(y, 0, bytes, s), "memset y");
+  CUDA_TRY(launch_expand(p->d_ya, p->d_act, y, p->n_active, s), "expand launch");
+  return STTSV_OK;
+}
+
 extern "C" sttsv_status_t sttsv_apply(sttsv_plan_t p, const double* x, double* y, void* stream) {
   if (!p || !x || !y) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
   const size_t bytes = (size_t)p->n * sizeof(double);
@@ -785,12 +817,7 @@ extern "C" sttsv_status_t sttsv_apply(sttsv_plan_t p, const double* x, double* y
   sttsv_status_t st = check_async(p);
   if (st != STTSV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, s), "gather launch");
-  st = apply_active(p, s);
-  if (st != STTSV_OK) return st;
-  CUDA_TRY(cudaMemsetAsync(y, 0, bytes, s), "memset y");
-  CUDA_TRY(launch_expand(p->d_ya, p->d_act, y, p->n_active, s), "expand launch");
-  return STTSV_OK;
+  return apply_dense(p, x, y, s);
 }
 
 extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host, double* y_host) {
