@@ -147,10 +147,10 @@ __device__ __forceinline__ void dp_edge_table(const double* const (&rows)[K], do
 // operations instead of L(L+1)/2); the scalar prefix / suffix products of the
 // x_u are carried separately.  Used for ranks N >= 11 (L up to N-1).
 
-// r = (a*b) mod t^L with a[0] = b[0] = r[0] = 1
+// r = (a*b) mod t^L with a[0] = b[0] = r[0] = 1: slot 0 of a normalised series
+// is never read or written (the leading 1 stays implicit, no register moves)
 template <int L>
 __device__ __forceinline__ void trunc_mul_norm(const double (&a)[L], const double (&b)[L], double (&r)[L]) {
-  r[0] = 1.0;
 #pragma unroll
   for (int j = 1; j < L; ++j) {
     double s = a[j] + b[j];
@@ -185,17 +185,16 @@ __device__ __forceinline__ void dp_edge_table_norm(const double* const (&rows)[K
     if constexpr (D == 1) F = x;
     if constexpr (D >= 2) F = x * __ldg(rows[0] + (D - 1));
   } else {
-    double h[K][L], x[K];
+    double h[K][L], x[K];  // h[i][0] holds x_i (slot 0 of a normalised series is implicit 1)
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       load_series<L>(rows[i], h[i]);
       x[i] = h[i][0];
-      h[i][0] = 1.0;
     }
     if constexpr (K == 2) {
       if constexpr (D >= 1) F = x[0] * x[1] * coef_n<D - 1, L>(h[0], h[1]);
-      q[0] = x[1] * h[1][D];
-      q[1] = x[0] * h[0][D];
+      q[0] = D == 0 ? x[1] : x[1] * h[1][D];
+      q[1] = D == 0 ? x[0] : x[0] * h[0][D];
     } else {
       double P[K - 2][L], Xp[K - 2];
 #pragma unroll
@@ -225,7 +224,7 @@ __device__ __forceinline__ void dp_edge_table_norm(const double* const (&rows)[K
           q[0] = x[1] * Xs * coef_n<D, L>(h[1], S);
         }
       }
-      if constexpr (K == 3) q[0] = Xs * S[D];
+      if constexpr (K == 3) q[0] = D == 0 ? Xs : Xs * S[D];
     }
   }
 }

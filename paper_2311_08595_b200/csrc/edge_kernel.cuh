@@ -446,7 +446,7 @@ __device__ __forceinline__ void edge_big(int K, const int32_t* __restrict__ sid,
 // separately (prefix product X on the stack row's slot 0, suffix product Xs).
 // Every term is still a product of positive numbers for x > 0.
 
-// a = (a*b) mod t^L for a[0] = b[0] = 1 (slot 0 untouched), in place
+// a = (a*b) mod t^L for a[0] = b[0] = 1 (slot 0 never read or written), in place
 template <int L>
 __device__ __forceinline__ void trunc_mul_norm_inplace(double (&a)[L], const double (&b)[L]) {
 #pragma unroll
@@ -472,13 +472,12 @@ __device__ __forceinline__ double coef_norm(const double (&a)[L], const double (
   }
 }
 
-// load a normalised row: returns x, fills h[0] = 1, h[1..L-1]
+// load a normalised row: returns x (slot 0), fills h[1..L-1]; h[0] is not a
+// coefficient (the leading 1 stays implicit)
 template <int L>
 __device__ __forceinline__ double load_norm(const double* __restrict__ row, double (&h)[L]) {
   load_series<L>(row, h);
-  const double x = h[0];
-  h[0] = 1.0;
-  return x;
+  return h[0];
 }
 
 template <int L, int TILE, int NT, int RB, bool DET>
@@ -506,8 +505,8 @@ __device__ __forceinline__ void edge_big_norm(int K, const int32_t* __restrict__
     double F = 0.0;
     if constexpr (D >= 1) F = xa * xb * coef_norm<D - 1, L>(a, b);
     const double wF = w * F;
-    dep(0, sid[0], fma(w, xb * b[D], wF));   // g_1[D] = x_1 h_1[D]
-    dep(1, sid[TILE], fma(w, xa * a[D], wF));
+    dep(0, sid[0], fma(w, D == 0 ? xb : xb * b[D], wF));   // g_1[D] = x_1 h_1[D]
+    dep(1, sid[TILE], fma(w, D == 0 ? xa : xa * a[D], wF));
     return;
   }
   double cur[L], g[L], S[L];
@@ -543,7 +542,6 @@ __device__ __forceinline__ void edge_big_norm(int K, const int32_t* __restrict__
       Xp = stk[((i - 1) * L) * NT];
 #pragma unroll
       for (int j = 1; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];  // pop (X_{i-1}, P_{i-1})
-      cur[0] = 1.0;
     } else {
       Xp = load_norm<L>(row(0), cur);  // P_0 = h_0 (the hottest row: L1-resident)
     }
@@ -555,7 +553,7 @@ __device__ __forceinline__ void edge_big_norm(int K, const int32_t* __restrict__
       dep(0, sid[0], fma(w, xi * Xs * coef_norm<D, L>(g, S), wF));  // [t^D] g_1 S_2
     }
   }
-  if (K == 3) dep(0, sid[0], fma(w, Xs * S[D], wF));  // S_1 = x_1 x_2 (h_1 h_2)
+  if (K == 3) dep(0, sid[0], fma(w, D == 0 ? Xs : Xs * S[D], wF));  // S_1 = x_1 x_2 (h_1 h_2)
 }
 
 template <int L, int LMAX, int TILE, int NT, int RB, bool DET>
