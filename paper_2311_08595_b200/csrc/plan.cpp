@@ -2,12 +2,14 @@
 //
 // sttsv_plan_create validates the IOU hyperedges,
 // computes global degrees, relabels active vertices by descending degree
-// (hot vertices get small ids, which the kernel's scatter tiers key on),
-// buckets the edges of this shard by cardinality into SoA int32 id columns,
-// folds the per-size constant (N-1)!/|beta(k)| = (N-1)!/(k! S(N,k))
-// (PAPER.md:342 footnote, Alg. 2 factor PAPER.md:391) into the fp64 weights,
-// and uploads everything once.  sttsv_apply is then gather -> edge kernel ->
-// (NCCL allreduce) -> expand, all on the caller's stream.
+// (hot vertices get small ids: the kernel's per-CTA hot slices key on them),
+// buckets the edges of this shard by cardinality into SoA int32 id columns
+// sorted lexicographically and padded to whole tiles, folds the per-size
+// constant (N-1)!/|beta(k)| = (N-1)!/(k! S(N,k)) (PAPER.md:342 footnote,
+// Alg. 2 factor PAPER.md:391) into the fp64 weights, optionally merges
+// duplicate edges or builds the deterministic slot map, and uploads
+// everything once.  sttsv_apply is then gather -> edge kernel -> (NCCL
+// allreduce) -> expand, all on the caller's stream.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -459,7 +461,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   }
   // Sort each bucket lexicographically (stable: the plan is deterministic).
   // Consecutive edges then share their hot low slots, which the kernel's
-  // warp-segmented scatter turns into one deposit per run.
+  // per-lane run accumulators turn into one deposit per run.
   for (int k = 1; k <= N; ++k) {
     if (mk[k] == 0) continue;
     const int32_t* R = rows.data() + row_off[k];
@@ -511,7 +513,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<double>().swap(wrow);
   std::vector<int32_t>().swap(newid);
 
-  // ---- tile order: buckets most expensive first; CTAs get contiguous cost-balanced tile ranges
+  // ---- tile order: buckets most expensive first (the dynamic scheduler's tail is the cheapest work)
   int occ = 0;
   const int H = (int)std::min<int64_t>(na, 4096);
   const int T = p->ent.run_slots;
