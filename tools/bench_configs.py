@@ -124,6 +124,15 @@ def main():
             rec["power50_ms"] = med50
             rec["power50_ms_per_iter"] = med50 / 50
             rec["power50_incidences_per_s"] = 50 * hg.incidences / (med50 * 1e-3)
+            # f1: Alg. 1 (NQZ) to convergence of the lambda bracket
+            for tau in (1e-6, 1e-9):
+                xh = x0.clone()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, _, lo, hi, its = plan.hec(xh, tau, 2000, z)
+                torch.cuda.synchronize()
+                rec["hec_tau%g" % tau] = {"iters": its, "seconds": time.perf_counter() - t0, "lambda_min": lo,
+                                          "lambda_max": hi, "gap": (hi - lo) / lo}
         line = json.dumps(rec)
         print(line, flush=True)
         if out:
