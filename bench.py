@@ -261,9 +261,10 @@ def run_ours(args):
     sparse_x = info["n_active"] * 8 <= hg.n   # sttsv_apply_host copies only x on the active vertices
     e2e = {"value": hg.incidences / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(info["n_active"] * 8 if sparse_x else xh.numel() * 8),
-           "d2h_bytes_per_step": int(yh.numel() * 8), "ms_per_step": e2e_s * 1e3,
-           "timing": "host perf_counter around synchronous sttsv_apply_host (pinned buffers; x gathered on the "
-                     "host to the %d active vertices)" % info["n_active"] if sparse_x else
+           "d2h_bytes_per_step": int(info["n_active"] * 8 if sparse_x else yh.numel() * 8), "ms_per_step": e2e_s * 1e3,
+           "timing": "host perf_counter around synchronous sttsv_apply_host (pinned buffers; only the %d active "
+                     "entries of x and y cross PCIe, the host zero-fills y during the GPU work)" % info["n_active"]
+                     if sparse_x else
                      "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
 
     # ---------------- roofline of the dominant kernel (edge kernel)

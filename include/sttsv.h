@@ -139,10 +139,11 @@ sttsv_status_t sttsv_apply_batch(sttsv_plan_t plan, const double* X_dev, double*
                                  void* stream);
 
 /* sttsv_apply_host — the same product from HOST vectors, synchronous.  When the
- * active set is sparse (n_active <= n/8) only x on the active vertices crosses
- * PCIe (gathered on the host into a pinned buffer); otherwise all of x (fp64[n])
- * is copied.  y (fp64[n]) is copied back in full.  Host buffers may be
- * pageable; a pinned y is faster. */
+ * active set is sparse (n_active <= n/8) only the active parts cross PCIe: x is
+ * gathered on the host into a pinned buffer (n_active doubles in), y_a comes
+ * back (n_active doubles out) and the host zero-fills y (overlapping the GPU
+ * work) and scatters y_a into it.  Otherwise x and y (fp64[n]) are copied in
+ * full.  Host buffers may be pageable. */
 sttsv_status_t sttsv_apply_host(sttsv_plan_t plan, const double* x_host, double* y_host);
 
 /* sttsv_power_iterate — the x-update of Alg. 1 (NQZ, PAPER.md:351-355 lines 3-6),

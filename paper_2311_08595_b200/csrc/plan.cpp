@@ -831,30 +831,43 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
   if (overlap(x_host, bytes, y_host, bytes)) return fail(STTSV_ERR_ALIAS, "x and y overlap");
   DeviceGuard g(p->device);
   if (!p->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->host_stream, cudaStreamNonBlocking), "stream");
-  if (!p->d_xhost) {
-    CUDA_TRY(cudaMalloc(&p->d_xhost, 2 * bytes), "cudaMalloc e2e staging");
-    p->d_yhost = p->d_xhost + p->n;
-  }
   cudaStream_t s = p->host_stream;
   const int64_t na = p->n_active;
   if (na > 0 && na * 8 <= p->n) {
-    // sparse active set: only x on the active vertices crosses PCIe.  Gather it
-    // on the host (OpenMP) into a pinned buffer, copy n_a doubles, build the
-    // series table from it, apply, expand, copy y back.
-    if (!p->h_xa) CUDA_TRY(cudaMallocHost(&p->h_xa, (size_t)na * sizeof(double)), "cudaMallocHost x_a");
+    // sparse active set: only the active parts of x and y cross PCIe.  Gather x
+    // on the host (OpenMP) into a pinned buffer, copy n_a doubles in, build the
+    // series table, apply, copy y_a out; the host zero-fills y while the GPU
+    // computes, then scatters y_a (y is 0 off the active set: a
+    // vertex in no hyperedge gets no tensor entry).
+    if (!p->h_xa) CUDA_TRY(cudaMallocHost(&p->h_xa, 2 * (size_t)na * sizeof(double)), "cudaMallocHost x_a/y_a");
     const int32_t* act = p->h_act.data();
     double* xa = p->h_xa;
+    double* ya = p->h_xa + na;
 #pragma omp parallel for schedule(static) if (na > 16384)
     for (int64_t i = 0; i < na; ++i) xa[i] = x_host[act[i]];
     sttsv_status_t st0 = check_async(p);
     if (st0 != STTSV_OK) return st0;
-    CUDA_TRY(cudaMemcpyAsync(p->d_xa, p->h_xa, (size_t)na * sizeof(double), cudaMemcpyHostToDevice, s), "H2D x_a");
+    CUDA_TRY(cudaMemcpyAsync(p->d_xa, xa, (size_t)na * sizeof(double), cudaMemcpyHostToDevice, s), "H2D x_a");
     CUDA_TRY(launch_series(p->d_xa, p->d_xg, p->gs, p->ent.table_norm, na, s), "series launch");
     sttsv_status_t st = apply_active(p, s);
     if (st != STTSV_OK) return st;
-    CUDA_TRY(cudaMemsetAsync(p->d_yhost, 0, bytes, s), "memset y");
-    CUDA_TRY(launch_expand(p->d_ya, p->d_act, p->d_yhost, na, s), "expand launch");
-  } else {
+    CUDA_TRY(cudaMemcpyAsync(ya, p->d_ya, (size_t)na * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H y_a");
+    const int64_t n = p->n;
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+    for (int64_t c = 0; c < (n + 65535) / 65536; ++c) {
+      const int64_t a = c * 65536, b = std::min<int64_t>(n, a + 65536);
+      memset(y_host + a, 0, (size_t)(b - a) * sizeof(double));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+#pragma omp parallel for schedule(static) if (na > 16384)
+    for (int64_t i = 0; i < na; ++i) y_host[act[i]] = ya[i];
+    return STTSV_OK;
+  }
+  if (!p->d_xhost) {
+    CUDA_TRY(cudaMalloc(&p->d_xhost, 2 * bytes), "cudaMalloc e2e staging");
+    p->d_yhost = p->d_xhost + p->n;
+  }
+  {
     CUDA_TRY(cudaMemcpyAsync(p->d_xhost, x_host, bytes, cudaMemcpyHostToDevice, s), "H2D x");
     sttsv_status_t st = sttsv_apply(p, p->d_xhost, p->d_yhost, s);
     if (st != STTSV_OK) return st;
