@@ -18,7 +18,7 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.fn_det = (const void*)edge_kernel<STTSV_INST_N, false, true>;
   e.block = EdgeCfg<STTSV_INST_N>::THREADS;
   e.tile = EdgeCfg<STTSV_INST_N>::TILE;
-  e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::STAGES * EdgeCfg<STTSV_INST_N>::STAGE_BYTES;
+  e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::RING_BYTES;
   e.rank = STTSV_INST_N;
   e.run_slots = EdgeCfg<STTSV_INST_N>::RMAX;
   e.big = EdgeCfg<STTSV_INST_N>::BIG ? (STTSV_BIG_LOCAL ? 2 : 1) : 0;

@@ -11,7 +11,7 @@
 // CTA are mostly neighbours in the sort order.
 //
 // Warp specialisation.  Per CTA, one producer warp streams tiles into an
-// STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk ->
+// shared-memory byte ring (each stage sized by its bucket's k) with 1-D TMA bulk copies (cp.async.bulk ->
 // SASS UBLKCP, completion on a `full` mbarrier with expect_tx) and publishes the
 // tile index in the stage; NCW consumer warps each take a block of 32*EPL edges
 // of the tile, lane l the EPL CONSECUTIVE edges l*EPL .. l*EPL+EPL-1 (EPL odd:
@@ -127,12 +127,17 @@ struct EdgeCfg {
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
-  static constexpr int STAGE_BYTES = TILE * EDGE_BYTES;
+  static constexpr int STAGE_BYTES = TILE * EDGE_BYTES;     // largest stage (k = KMAX)
   static constexpr int STAGES_FIT = RING_BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
+  // byte ring: a stage takes TILE*(4k+8) bytes of its bucket's k, so small-k
+  // tiles are more deep in flight; SLOTS bounds the stages in flight
+  static constexpr int RING_BYTES = (STAGES * STAGE_BYTES > RING_BUDGET ? STAGES * STAGE_BYTES : RING_BUDGET) / 128 * 128;
+  static constexpr int SLOTS = 8;
   static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = BIG ? 1 : (N <= 10 ? STTSV_MIN_BLOCKS : STTSV_MID_BLOCKS);
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
+  static_assert(RING_BYTES >= 2 * STAGE_BYTES, "ring must hold two of the largest stages");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
 };
 
@@ -582,24 +587,26 @@ template <int N, bool BATCH, bool DET>
 __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     edge_kernel(const __grid_constant__ EdgeKernelParams p) {
   using Cfg = EdgeCfg<N>;
-  constexpr int TILE = Cfg::TILE, STAGES = Cfg::STAGES, KMAX = Cfg::KMAX, NCW = Cfg::NCW, EPL = Cfg::EPL;
+  constexpr int TILE = Cfg::TILE, KMAX = Cfg::KMAX, NCW = Cfg::NCW, EPL = Cfg::EPL;
   constexpr int RMAX = Cfg::RMAX;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // layout: [STAGES][ ids KMAX*TILE int32 | w TILE f64 ] | (large-rank path) prefix
+  // layout: byte ring of stages [ ids k*TILE int32 | w TILE f64 ] | (large-rank path) prefix
   // stacks [p.stack_doubles][NCW*32] f64, thread-interleaved
   unsigned char* ring = smem_raw;
-  double* stack = reinterpret_cast<double*>(smem_raw + STAGES * Cfg::STAGE_BYTES);
+  double* stack = reinterpret_cast<double*>(smem_raw + Cfg::RING_BYTES);
   // batch (f4): vector v uses xg + v*xg_vstride, ya + v*ya_vstride, priv slice + v*H
   const int nvec = BATCH ? p.nvec : 1;
   double* const priv_cta = p.priv + (size_t)blockIdx.x * p.H * nvec;
   const Sink sk{priv_cta, p.ya, p.H};
-  __shared__ uint64_t full[STAGES], empty[STAGES];
+  constexpr int SLOTS = Cfg::SLOTS;
+  __shared__ uint64_t full[SLOTS], empty[SLOTS];
+  __shared__ uint32_t soff[SLOTS];  // byte offset of each slot's stage in the ring
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ int64_t stile[STAGES];  // tile index staged in each slot (-1: no more work)
+  __shared__ int64_t stile[SLOTS];  // tile index staged in each slot (-1: no more work)
 
   for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) priv_cta[j] = 0.0;
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < SLOTS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
@@ -608,34 +615,52 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   __syncthreads();
 
   if (warp == NCW) {
-    // ---------------- producer warp: grab chunks of tiles, TMA bulk copies of tile t into
-    // stage it % STAGES, publish t in stile[s] (ordered by the mbarrier's release)
+    // ---------------- producer warp: grab chunks of tiles; each tile's stage is
+    // TILE*(4k+8) bytes carved FIFO out of the byte ring (wrapping to offset 0
+    // when the tail of the ring is too short); slot it % SLOTS carries its
+    // offset and tile index (published before the mbarrier's release)
     if (lane == 0) {
       int b = 0;
       int64_t ct = 0, ce = 0;
+      uint64_t head = 0, tail = 0;  // ring positions (monotonic; offset = pos % RING_BYTES)
+      uint64_t endpos[SLOTS];       // ring position just past each in-flight slot's stage
+      int64_t oldest = 0;           // oldest iteration whose stage may still be in use
       for (int64_t it = 0;; ++it) {
-        const int s = (int)(it % STAGES);
-        if (it >= STAGES) mbar_wait_sleep(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+        const int s = (int)(it % SLOTS);
         if (ct == ce) {
           ct = (int64_t)atomicAdd(p.tile_counter, 1ull) * p.chunk;
           ce = ct + p.chunk < p.num_tiles ? ct + p.chunk : p.num_tiles;
         }
-        if (ct >= p.num_tiles) {
-          stile[s] = -1;
+        const int64_t t = ct < p.num_tiles ? ct++ : -1;
+        if (t >= 0)
+          while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
+        const int k = t >= 0 ? p.b[b].k : 0;
+        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (4 * k + 8)) : 0u;
+        uint64_t start = head;
+        if (start % Cfg::RING_BYTES + need > (uint64_t)Cfg::RING_BYTES) start += Cfg::RING_BYTES - start % Cfg::RING_BYTES;
+        while (it - oldest >= SLOTS || (oldest < it && start + need - tail > (uint64_t)Cfg::RING_BYTES)) {
+          const int so = (int)(oldest % SLOTS);
+          mbar_wait_sleep(&empty[so], (uint32_t)((oldest / SLOTS) & 1));
+          tail = endpos[so];
+          ++oldest;
+        }
+        endpos[s] = start + need;
+        head = start + need;
+        const uint32_t off = (uint32_t)(start % Cfg::RING_BYTES);
+        soff[s] = off;
+        stile[s] = t;
+        if (t < 0) {
           mbar_arrive_expect_tx(&full[s], 0);
           break;
         }
-        const int64_t t = ct++;
-        while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const BucketDesc& bd = p.b[b];
         const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
         constexpr uint32_t id_bytes = TILE * 4, w_bytes = TILE * 8;
-        unsigned char* st = ring + s * Cfg::STAGE_BYTES;
-        stile[s] = t;
-        mbar_arrive_expect_tx(&full[s], id_bytes * bd.k + w_bytes);
-        for (int i = 0; i < bd.k; ++i)
+        unsigned char* st = ring + off;
+        mbar_arrive_expect_tx(&full[s], need);
+        for (int i = 0; i < k; ++i)
           bulk_g2s(st + i * TILE * 4, p.ids + bd.ids_off + i * bd.stride + e0, id_bytes, &full[s]);
-        bulk_g2s(st + KMAX * TILE * 4, p.w + bd.w_off + e0, w_bytes, &full[s]);
+        bulk_g2s(st + k * TILE * 4, p.w + bd.w_off + e0, w_bytes, &full[s]);
       }
     }
   } else {
@@ -656,29 +681,29 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     const long long c_start = clock64();
 #endif
     for (int64_t it = 0;; ++it) {
-      const int s = (int)(it % STAGES);
+      const int s = (int)(it % SLOTS);
       const int base = warp * 32 * EPL;
 #if STTSV_WAITPROF
       const long long w0 = clock64();
-      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      mbar_wait(&full[s], (uint32_t)((it / SLOTS) & 1));
       wait_cyc += clock64() - w0;
 #else
-      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      mbar_wait(&full[s], (uint32_t)((it / SLOTS) & 1));
 #endif
       const int64_t t = stile[s];
       if (t < 0) break;
       any = true;
       while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
       const int k = p.b[b].k;
-#if STTSV_WAITPROF
+#if STTSV_WAITPROF > 1
       const long long kc0 = clock64();
 #endif
       const DetSink ds{DET ? p.slot + p.b[b].ids_off + (t - p.b[b].tile_begin) * TILE : nullptr, p.b[b].stride,
                        p.contrib};
       {
-        const unsigned char* st = ring + s * Cfg::STAGE_BYTES;
+        const unsigned char* st = ring + soff[s];
         const int32_t* sids = reinterpret_cast<const int32_t*>(st);
-        const double* sw = reinterpret_cast<const double*>(st + KMAX * TILE * 4);
+        const double* sw = reinterpret_cast<const double*>(st + k * TILE * 4);
         // one pass per vector; with several vectors the runs of a pass are flushed
         // (warp-aggregated) at its end, with one they continue across tiles
         for (int v = 0; v < nvec; ++v) {
@@ -707,7 +732,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         }
       }
       __syncwarp();
-#if STTSV_WAITPROF
+#if STTSV_WAITPROF > 1
       if (lane == 0) {
         atomicAdd(&g_k_cycles[2 * k], (unsigned long long)(clock64() - kc0));
         atomicAdd(&g_k_cycles[2 * k + 1], 1ull);
