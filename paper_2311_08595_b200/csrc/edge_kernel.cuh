@@ -628,8 +628,11 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
       for (int64_t it = 0;; ++it) {
         const int s = (int)(it % SLOTS);
         if (ct == ce) {
-          ct = (int64_t)atomicAdd(p.tile_counter, 1ull) * p.chunk;
-          ce = ct + p.chunk < p.num_tiles ? ct + p.chunk : p.num_tiles;
+          // guided: chunks of p.chunk tiles, single tiles once the counter passes
+          // p.guided_from (the tail is split finely across the CTAs)
+          const int64_t want = ct < p.guided_from ? p.chunk : 1;
+          ct = (int64_t)atomicAdd(p.tile_counter, (unsigned long long)want);
+          ce = ct + want < p.num_tiles ? ct + want : p.num_tiles;
         }
         const int64_t t = ct < p.num_tiles ? ct++ : -1;
         if (t >= 0)

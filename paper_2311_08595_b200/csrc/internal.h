@@ -52,6 +52,7 @@ struct EdgeKernelParams {
   int64_t num_tiles;
   unsigned long long* tile_counter;  // chunk counter of the dynamic tile scheduler (zeroed per launch)
   int64_t chunk;         // tiles per grab
+  int64_t guided_from;   // tile index after which grabs are single tiles
 };
 
 // Ranks with a fully unrolled edge kernel (one object file each); every other

@@ -570,6 +570,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   // cheapest bucket) balances: about 1/16 of a CTA's fair share
   kp.chunk = std::max<int64_t>(1, tiles / (grid * 16));
   if (const char* env = getenv("STTSV_CHUNK")) kp.chunk = std::max(1, atoi(env));
+  // the last ~2 chunks' worth per CTA is handed out one tile at a time
+  kp.guided_from = std::max<int64_t>(0, tiles - grid * kp.chunk * 2);
+  if (const char* env = getenv("STTSV_GUIDED")) kp.guided_from = std::max<int64_t>(0, tiles - grid * kp.chunk * atoi(env));
 
   // ---- deterministic mode: every stored incidence gets a slot in a vertex-major
   // buffer (vertex v's incidences in bucket / edge / member order), and each
