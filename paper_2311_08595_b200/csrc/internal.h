@@ -97,6 +97,8 @@ constexpr int kDetChunk = 4096;  // contributions per deterministic reduction ch
 // norm: series table format (dp.cuh series_row; EdgeKernelEntry::table_norm)
 cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
                           int64_t n_active, cudaStream_t s);
+cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
+                            int64_t n_active, double* ya, unsigned long long* counter, cudaStream_t s);
 cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)

@@ -27,6 +27,20 @@ __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __res
   }
 }
 
+// gather + series table + y_a = 0 + tile counter = 0 in one launch (sttsv_apply)
+__global__ void prologue_kernel(const double* __restrict__ x, const int32_t* __restrict__ act,
+                                double* __restrict__ xa, double* __restrict__ xg, int gs, int norm, int64_t n_active,
+                                double* __restrict__ ya, unsigned long long* __restrict__ counter) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[act[i]];
+    xa[i] = v;
+    series_row(v, xg + i * gs, gs, norm);
+    ya[i] = 0.0;
+  }
+}
+
 // series table rows from x_a (sttsv_apply_host's host-gathered path)
 __global__ void series_kernel(const double* __restrict__ xa, double* __restrict__ xg, int gs, int norm,
                               int64_t n_active) {
@@ -258,6 +272,12 @@ cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, doubl
                           int64_t n_active, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
   gather_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, norm, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
+                            int64_t n_active, double* ya, unsigned long long* counter, cudaStream_t s) {
+  prologue_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, norm, n_active, ya, counter);
   return cudaGetLastError();
 }
 

@@ -755,9 +755,10 @@ static sttsv_status_t check_async(sttsv_plan_s* p) {
 }
 
 // y_a = (B x_a^{N-1}) on the active vertices (x_a already gathered)
-static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
+// zeroed: the prologue kernel already cleared y_a and the tile counter
+static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed = false) {
   if (p->n_active == 0) return STTSV_OK;
-  if (!p->det) CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
+  if (!p->det && !zeroed) CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
   if (p->kp.num_tiles > 0) {
     std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
     if (p->profiling) {
@@ -770,7 +771,8 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s) {
       ev = &p->events[p->events_used++];
       CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
     }
-    CUDA_TRY(cudaMemsetAsync(p->kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
+    if (!zeroed)
+      CUDA_TRY(cudaMemsetAsync(p->kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
     CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0), "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }
@@ -808,8 +810,10 @@ static sttsv_status_t apply_dense(sttsv_plan_s* p, const double* x, double* y, c
     CUDA_TRY(cudaMemsetAsync(y, 0, bytes, p->side), "memset y");
     CUDA_TRY(cudaEventRecord(p->ev_join, p->side), "join record");
   }
-  CUDA_TRY(launch_gather(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, s), "gather launch");
-  sttsv_status_t st = apply_active(p, s);
+  // one prologue launch: gather x_a, series table, y_a = 0, tile counter = 0
+  CUDA_TRY(launch_prologue(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, p->d_ya,
+                           p->kp.tile_counter, s), "prologue launch");
+  sttsv_status_t st = apply_active(p, s, true);
   if (st != STTSV_OK) return st;
   if (fork) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0), "join wait");
   else CUDA_TRY(cudaMemsetAsync(y, 0, bytes, s), "memset y");
