@@ -27,14 +27,15 @@ __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __res
   }
 }
 
-// gather + series table + y_a = 0 + tile counter = 0 in one launch (sttsv_apply)
-__global__ void prologue_kernel(const double* __restrict__ x, const int32_t* __restrict__ act,
-                                double* __restrict__ xa, double* __restrict__ xg, int gs, int norm, int64_t n_active,
+// gather + series table + y_a = 0 + tile counter = 0 in one launch (sttsv_apply;
+// sttsv_apply_host passes act = nullptr with x = the host-gathered x_a)
+__global__ void prologue_kernel(const double* x, const int32_t* __restrict__ act,
+                                double* xa, double* __restrict__ xg, int gs, int norm, int64_t n_active,
                                 double* __restrict__ ya, unsigned long long* __restrict__ counter) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0ull;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = x[act[i]];
+    const double v = act ? x[act[i]] : x[i];  // act == nullptr: x is already x_a
     xa[i] = v;
     series_row(v, xg + i * gs, gs, norm);
     ya[i] = 0.0;

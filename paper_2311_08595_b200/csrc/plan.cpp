@@ -855,8 +855,9 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
     sttsv_status_t st0 = check_async(p);
     if (st0 != STTSV_OK) return st0;
     CUDA_TRY(cudaMemcpyAsync(p->d_xa, xa, (size_t)na * sizeof(double), cudaMemcpyHostToDevice, s), "H2D x_a");
-    CUDA_TRY(launch_series(p->d_xa, p->d_xg, p->gs, p->ent.table_norm, na, s), "series launch");
-    sttsv_status_t st = apply_active(p, s);
+    CUDA_TRY(launch_prologue(p->d_xa, nullptr, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, na, p->d_ya,
+                             p->kp.tile_counter, s), "prologue launch");
+    sttsv_status_t st = apply_active(p, s, true);
     if (st != STTSV_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(ya, p->d_ya, (size_t)na * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H y_a");
     const int64_t n = p->n;
