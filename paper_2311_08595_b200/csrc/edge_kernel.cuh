@@ -61,7 +61,7 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 
 // ---- compile-time tuning (each default was chosen by A/B timing on B200 with
 // tools/variants.py + tools/time_apply.py)
-// small ranks (N <= 10): two CTAs per SM, each 7 consumer warps + 1 producer
+// small ranks (N <= 10): two CTAs per SM, each 8 (N <= 8) or 7 consumer warps + 1 producer
 // with a 110 KB ring (two independent TMA pipelines per SM measured 2.7% faster
 // than one CTA of 15 consumers on `large`), 5 edges per lane per tile
 #ifndef STTSV_EPL
@@ -71,7 +71,11 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #define STTSV_RING_KB 110
 #endif
 #ifndef STTSV_NCW_SMALL
-#define STTSV_NCW_SMALL 7
+#define STTSV_NCW_SMALL 8
+#endif
+// N = 9, 10: 7 consumer warps (8 would spill under the two-CTA register cap)
+#ifndef STTSV_NCW_SMALL9
+#define STTSV_NCW_SMALL9 7
 #endif
 #ifndef STTSV_MIN_BLOCKS
 #define STTSV_MIN_BLOCKS 2
@@ -123,7 +127,7 @@ struct EdgeCfg {
   // consumer warps per CTA (NCW_PREF), fewer when two stages of the largest
   // bucket would not fit the ring budget
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
-  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 10 ? STTSV_NCW_SMALL : STTSV_NCW_MID);
+  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 8 ? STTSV_NCW_SMALL : N <= 10 ? STTSV_NCW_SMALL9 : STTSV_NCW_MID);
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
@@ -185,6 +189,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     if (ok) return;
   }
 }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -679,6 +684,9 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
     }
     int b = 0;
     bool any = false;
+    // programmatic dependent launch: x_a, the series table and y_a are written
+    // by the prologue grid (no-op when launched without the PDL attribute)
+    griddep_wait();
 #if STTSV_WAITPROF
     long long wait_cyc = 0;
     const long long c_start = clock64();
@@ -759,11 +767,21 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
   }
   // this CTA's reds into priv are ordered before the reads below (fence + barrier);
   // the reads go to L2 (ld.cg), where the reds were performed
+  if (warp == NCW) griddep_wait();  // the producer warp also adds into y_a below
   __threadfence();
   __syncthreads();
   for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) {
     const double v = __ldcg(priv_cta + j);
     if (v != 0.0) red_add(p.ya + (size_t)(j / p.H) * p.ya_vstride + j % p.H, v);
+  }
+  // the last CTA to finish resets the scheduler counters for the next launch
+  // (every producer has stopped taking tiles once all CTAs have counted in)
+  if (tid == 0) {
+    const unsigned long long done = atomicAdd(p.tile_counter + 1, 1ull);
+    if (done == gridDim.x - 1) {
+      p.tile_counter[0] = 0ull;
+      p.tile_counter[1] = 0ull;
+    }
   }
 }
 

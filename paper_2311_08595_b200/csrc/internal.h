@@ -50,7 +50,10 @@ struct EdgeKernelParams {
   int32_t H;             // ids < H accumulate in the CTA's private slice of priv
   int32_t tile_edges;    // edges per tile
   int64_t num_tiles;
-  unsigned long long* tile_counter;  // chunk counter of the dynamic tile scheduler (zeroed per launch)
+  // [0]: chunk counter of the dynamic tile scheduler, [1]: CTAs finished; both
+  // zero at launch (zeroed at plan creation; the last CTA of every launch
+  // resets them)
+  unsigned long long* tile_counter;
   int64_t chunk;         // tiles per grab
   int64_t guided_from;   // tile index after which grabs are single tiles
 };
@@ -86,9 +89,10 @@ size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N);
 // doubles of prefix stack per consumer thread of the large-rank path (edge_kernel.cuh)
 int edge_big_stack_doubles(int N);
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm);
-// mode: 0 one vector, 1 batch, 2 deterministic
+// mode: 0 one vector, 1 batch, 2 deterministic; pdl: programmatic dependent
+// launch (only directly behind launch_prologue on the same stream)
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
-                               cudaStream_t s, int mode = 0);
+                               cudaStream_t s, int mode = 0, bool pdl = false);
 // deterministic mode, pass 2: chunk sums (chunk c = contrib[cstart[c] .. cstart[c+1])) in a fixed
 // tree order, then y_a[v] = sum of v's chunks (vchunk[v] .. vchunk[v+1]) in order
 cudaError_t launch_det_reduce(const double* contrib, const int64_t* cstart, int64_t nchunks, double* csum,
@@ -98,7 +102,7 @@ constexpr int kDetChunk = 4096;  // contributions per deterministic reduction ch
 cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
                           int64_t n_active, cudaStream_t s);
 cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
-                            int64_t n_active, double* ya, unsigned long long* counter, cudaStream_t s);
+                            int64_t n_active, double* ya, cudaStream_t s);
 cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)

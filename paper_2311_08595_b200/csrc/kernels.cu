@@ -27,12 +27,16 @@ __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __res
   }
 }
 
-// gather + series table + y_a = 0 + tile counter = 0 in one launch (sttsv_apply;
-// sttsv_apply_host passes act = nullptr with x = the host-gathered x_a)
+// gather + series table + y_a = 0 in one launch (sttsv_apply; sttsv_apply_host
+// passes act = nullptr with x = the host-gathered x_a).  The edge kernel that
+// follows is a programmatic dependent launch: it may start (barrier setup,
+// private-slice zeroing, the first TMA stages of the edge stream) as soon as
+// every CTA here has started; its consumers wait (griddepcontrol.wait) for this
+// grid's completion before reading x_a / the series table / y_a.
 __global__ void prologue_kernel(const double* x, const int32_t* __restrict__ act,
                                 double* xa, double* __restrict__ xg, int gs, int norm, int64_t n_active,
-                                double* __restrict__ ya, unsigned long long* __restrict__ counter) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0ull;
+                                double* __restrict__ ya) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double v = act ? x[act[i]] : x[i];  // act == nullptr: x is already x_a
@@ -256,10 +260,22 @@ cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_b
 }
 
 cudaError_t launch_edge_kernel(const EdgeKernelEntry& e, const EdgeKernelParams& p, int grid, size_t smem,
-                               cudaStream_t s, int mode) {
+                               cudaStream_t s, int mode, bool pdl) {
   void* args[] = {const_cast<EdgeKernelParams*>(&p)};
   const void* fn = mode == 1 ? e.fn_batch : (mode == 2 ? e.fn_det : e.fn);
-  return cudaLaunchKernel(fn, dim3(grid), dim3(e.block), args, smem, s);
+  if (!pdl) return cudaLaunchKernel(fn, dim3(grid), dim3(e.block), args, smem, s);
+  // programmatic dependent launch behind the prologue kernel
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(e.block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 static int grid_for(int64_t n, int block, int cap) {
@@ -277,8 +293,8 @@ cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, doubl
 }
 
 cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
-                            int64_t n_active, double* ya, unsigned long long* counter, cudaStream_t s) {
-  prologue_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, norm, n_active, ya, counter);
+                            int64_t n_active, double* ya, cudaStream_t s) {
+  prologue_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(x, act, xa, xg, gs, norm, n_active, ya);
   return cudaGetLastError();
 }
 

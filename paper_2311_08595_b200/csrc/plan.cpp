@@ -656,6 +656,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.gs = gs;
   kp.ya = p->d_ya;
   kp.tile_counter = d_cnt;
+  if (ce == cudaSuccess) ce = cudaMemset(d_cnt, 0, 2 * sizeof(unsigned long long));
+  if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan counters"); }
   if (p->det) {
     const size_t a_slot = align(h_slot.size() * 4), a_con = align((det_total + 1) * 8),
                  a_cs = align(h_cstart.size() * 8), a_sum = align(p->det_chunks * 8 + 8), a_vc = align(h_vchunk.size() * 8);
@@ -755,7 +757,8 @@ static sttsv_status_t check_async(sttsv_plan_s* p) {
 }
 
 // y_a = (B x_a^{N-1}) on the active vertices (x_a already gathered)
-// zeroed: the prologue kernel already cleared y_a and the tile counter
+// zeroed: the prologue kernel, launched just before on `s`, cleared y_a; the
+// edge kernel is then a programmatic dependent launch (kernels.cu)
 static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed = false) {
   if (p->n_active == 0) return STTSV_OK;
   if (!p->det && !zeroed) CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
@@ -771,9 +774,8 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
       ev = &p->events[p->events_used++];
       CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
     }
-    if (!zeroed)
-      CUDA_TRY(cudaMemsetAsync(p->kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
-    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0), "edge kernel launch");
+    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed),
+             "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }
   if (p->det)  // fixed-order sums of the vertex-major buffer (every active vertex written)
@@ -810,9 +812,9 @@ static sttsv_status_t apply_dense(sttsv_plan_s* p, const double* x, double* y, c
     CUDA_TRY(cudaMemsetAsync(y, 0, bytes, p->side), "memset y");
     CUDA_TRY(cudaEventRecord(p->ev_join, p->side), "join record");
   }
-  // one prologue launch: gather x_a, series table, y_a = 0, tile counter = 0
-  CUDA_TRY(launch_prologue(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, p->d_ya,
-                           p->kp.tile_counter, s), "prologue launch");
+  // one prologue launch: gather x_a, series table, y_a = 0
+  CUDA_TRY(launch_prologue(x, p->d_act, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, p->n_active, p->d_ya, s),
+           "prologue launch");
   sttsv_status_t st = apply_active(p, s, true);
   if (st != STTSV_OK) return st;
   if (fork) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0), "join wait");
@@ -855,8 +857,8 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
     sttsv_status_t st0 = check_async(p);
     if (st0 != STTSV_OK) return st0;
     CUDA_TRY(cudaMemcpyAsync(p->d_xa, xa, (size_t)na * sizeof(double), cudaMemcpyHostToDevice, s), "H2D x_a");
-    CUDA_TRY(launch_prologue(p->d_xa, nullptr, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, na, p->d_ya,
-                             p->kp.tile_counter, s), "prologue launch");
+    CUDA_TRY(launch_prologue(p->d_xa, nullptr, p->d_xa, p->d_xg, p->gs, p->ent.table_norm, na, p->d_ya, s),
+             "prologue launch");
     sttsv_status_t st = apply_active(p, s, true);
     if (st != STTSV_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(ya, p->d_ya, (size_t)na * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H y_a");
@@ -1001,7 +1003,6 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       kp.ya = p->b_ya;
       kp.ya_vstride = na;
       kp.priv = p->b_priv;
-      CUDA_TRY(cudaMemsetAsync(kp.tile_counter, 0, sizeof(unsigned long long), s), "memset tile counter");
       CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0)),
                "edge kernel launch");
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,

@@ -32,6 +32,13 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 kms, kn = plan.profile_read()
+plan.profile(False)
+f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+f0.record()
+for _ in range(reps):
+    plan.apply(x, y)
+f1.record()
+torch.cuda.synchronize()
 err = float(((y - ref).abs().max() / ref.abs().max()).item())
 lib = S.load()
 if hasattr(lib, "sttsv_debug_wait"):
@@ -49,6 +56,6 @@ if hasattr(lib, "sttsv_debug_wait"):
             print("  k=%2d warp-tiles=%8d cycles share %5.1f%%  edges share %5.1f%%  cyc/warp-tile %.0f" % (
                 k, kb[2 * k + 1], 100.0 * kb[2 * k] / tot, 100.0 * info["edges_per_size"][k] / max(info["num_edges"], 1),
                 kb[2 * k] / kb[2 * k + 1]))
-print("%s lib=%s step_ms=%.4f kernel_ms=%.4f rerun_rel_diff=%.2e" % (
+print("%s lib=%s step_ms=%.4f step_ms_noprof=%.4f kernel_ms=%.4f rerun_rel_diff=%.2e" % (
     name, os.path.basename(os.environ.get("STTSV_LIB_PATH", "libsttsv.so")), e0.elapsed_time(e1) / reps,
-    kms / kn, err), flush=True)
+    f0.elapsed_time(f1) / reps, kms / kn, err), flush=True)
