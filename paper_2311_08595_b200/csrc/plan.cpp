@@ -515,7 +515,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
 
   // ---- tile order: buckets most expensive first (the dynamic scheduler's tail is the cheapest work)
   int occ = 0;
-  int hot = 512;  // ids below H accumulate in per-CTA L2 slices (STTSV_HOT overrides, for experiments;
+  int hot = 256;  // ids below H accumulate in per-CTA L2 slices (STTSV_HOT overrides, for experiments;
                   // 256-512 measured best: smaller slices are cheaper to zero and fold, 64 contends)
   if (const char* env = getenv("STTSV_HOT")) hot = std::max(0, atoi(env));
   const int H = (int)std::min<int64_t>(na, hot);

@@ -419,3 +419,72 @@ def test_fuzz(S, torch_cuda, seed):
         y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
     assert rel(y, ref) < TOL, (seed, N, n, m, flags, mode)
     plan.close()
+
+
+# ------------------------------- launch plumbing: PDL launches, scheduler counters
+@pytest.mark.parametrize("name,m,n", [("mid", 200_000, None), ("large", 300_000, 2_000_000), ("high-rank", 1_000, None)])
+def test_interleaved_entry_points(S, torch_cuda, name, m, n):
+    """One plan driven through every entry point in turn (PDL-launched applies, the
+    batch kernel, the host-buffer path, power steps, profiled applies): the dynamic
+    tile scheduler's counters are reset by the last CTA of each launch, so every
+    call must see all tiles exactly once."""
+    torch = torch_cuda
+    hg = W.generate(name, m=m, n=n)
+    plan = S.Plan.from_hypergraph(hg)
+    ref = oracle.sttsv(hg)
+    x = torch.from_numpy(hg.x).cuda()
+    rng = np.random.default_rng(7)
+    x2h = rng.uniform(0.05, 1.0, hg.n)
+    ref2 = oracle.sttsv(hg, x=x2h)
+    for rnd in range(2):
+        y = plan.apply(x)
+        torch.cuda.synchronize()
+        assert rel(y.cpu().numpy(), ref) < TOL, (rnd, "apply")
+        X = torch.stack([x, torch.from_numpy(x2h).cuda()])
+        Y = plan.apply_batch(X)
+        torch.cuda.synchronize()
+        assert rel(Y[0].cpu().numpy(), ref) < TOL and rel(Y[1].cpu().numpy(), ref2) < TOL, (rnd, "batch")
+        assert rel(plan.apply_host(x2h), ref2) < TOL, (rnd, "host")
+        plan.profile(True)
+        y = plan.apply(x)
+        y = plan.apply(x)
+        torch.cuda.synchronize()
+        plan.profile(False)
+        kms, kn = plan.profile_read()
+        assert kn >= 2 and kms > 0
+        assert rel(y.cpu().numpy(), ref) < TOL, (rnd, "profiled apply")
+        xx = x.clone()
+        plan.power_iterate(xx, 2)
+    plan.close()
+
+
+def test_apply_in_cuda_graph(S, torch_cuda):
+    """Applies captured in a CUDA graph (the edge kernel's programmatic dependency on
+    the prologue becomes a graph edge) and replayed with new inputs."""
+    torch = torch_cuda
+    hg = W.generate("mid", m=150_000)
+    plan = S.Plan.from_hypergraph(hg)
+    rng = np.random.default_rng(11)
+    xs = [rng.uniform(0.05, 1.0, hg.n) for _ in range(3)]
+    x = torch.from_numpy(xs[0]).cuda()
+    ys = [torch.empty_like(x) for _ in range(3)]
+    xin = [torch.from_numpy(v).cuda() for v in xs]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.apply(x, ys[0], s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(3):
+                x.copy_(xin[i])
+                plan.apply(x, ys[i], s)
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for yy in ys:
+            yy.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert rel(ys[i].cpu().numpy(), oracle.sttsv(hg, x=xs[i])) < TOL, (rep, i)
+    plan.close()
