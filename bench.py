@@ -313,29 +313,43 @@ def run_ours(args):
                   "note": "STTSV_MERGE_DUPLICATES plan (input incidences / time); not the headline"}
         mplan.close()
 
-    # ---------------- secondary: f4 batched apply (4 vectors share one pass over the edge stream)
+    # ---------------- secondary: f4 batched apply of 4 vectors, both strategies:
+    # the default (one single-vector pass per vector) and STTSV_BATCH_FUSED (one
+    # pass over the edge stream for all vectors)
     batch = None
     if not args.no_batch_report:
         nv = 4
         X = x.unsqueeze(0).repeat(nv, 1)
         Y = torch.empty_like(X)
-        for _ in range(args.warmup):
-            plan.apply_batch(X, Y, stream)
-        barrier()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0.record(stream)
-        for _ in range(args.steps):
-            plan.apply_batch(X, Y, stream)
-        b1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        bms = b0.elapsed_time(b1) / args.steps
-        if world > 1:
-            t = torch.tensor([bms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            bms = t.item()
+
+        def time_batch(pl):
+            for _ in range(args.warmup):
+                pl.apply_batch(X, Y, stream)
+            barrier()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(args.steps):
+                pl.apply_batch(X, Y, stream)
+            b1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            ms = b0.elapsed_time(b1) / args.steps
+            if world > 1:
+                t = torch.tensor([ms], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = t.item()
+            return ms
+
+        bms = time_batch(plan)
+        fplan = S.Plan.from_hypergraph(hg, device=local, world=world, rank=rank, comm=comm,
+                                       flags=S.STTSV_BATCH_FUSED)
+        fms = time_batch(fplan)
+        fplan.close()
+        del fplan
         batch = {"vectors": nv, "value": nv * hg.incidences / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms,
-                 "note": "sttsv_apply_batch (SURVEY.md f4): vector-incidences/s; not the headline"}
+                 "fused": {"value": nv * hg.incidences / (fms * 1e-3), "ms_per_step": fms},
+                 "note": "sttsv_apply_batch (SURVEY.md f4): vector-incidences/s; default = one pass per vector, "
+                         "fused = STTSV_BATCH_FUSED (one pass over the edge stream); not the headline"}
         del X, Y
 
     cpu = None

@@ -72,10 +72,13 @@ enum {
                                        repeated ids are still an error                             */
   STTSV_MERGE_DUPLICATES = 1u << 1, /* merge identical vertex sets of a shard, summing their weights
                                        (B is linear in w); the plan stores fewer edges */
-  STTSV_DETERMINISTIC = 1u << 2     /* bit-reproducible y: each contribution is stored to a
+  STTSV_DETERMINISTIC = 1u << 2,    /* bit-reproducible y: each contribution is stored to a
                                        plan-time slot of a vertex-major buffer and summed in a fixed order
                                        (no atomics); costs ~12 B more per incidence per apply, needs
-                                       < 2^31 incidences per shard; not with sttsv_apply_batch nvec > 1 */
+                                       < 2^31 incidences per shard; not with STTSV_BATCH_FUSED nvec > 1 */
+  STTSV_BATCH_FUSED = 1u << 3       /* sttsv_apply_batch runs ONE pass over the hyperedge stream for all
+                                       vectors (the fused batch kernel) instead of one sttsv_apply pass
+                                       per vector; see sttsv_apply_batch for when each is faster       */
 };
 
 /* ------------------------------------------------------------------ plans */
@@ -125,15 +128,23 @@ sttsv_status_t sttsv_plan_destroy(sttsv_plan_t plan);
  * With a comm the result is identical on all ranks (allreduce semantics). */
 sttsv_status_t sttsv_apply(sttsv_plan_t plan, const double* x_dev, double* y_dev, void* stream);
 
-/* sttsv_apply_batch — Y_v = B X_v^{N-1} for nvec vectors at once (SURVEY.md
- * §8(f) f4: the hyperedge stream is read once for all vectors; each vector's
- * DP and scatter run in turn on the staged tile).
+/* sttsv_apply_batch — Y_v = B X_v^{N-1} for nvec vectors.
  *  X_dev  device fp64, vector v at X_dev + v*ld (length n), read only.
  *  Y_dev  device fp64, same layout, overwritten; must not overlap X_dev.
  *  nvec   1 .. STTSV_MAX_BATCH;  ld >= n.
- * Stream-ordered like sttsv_apply; the first call with a larger nvec allocates a
- * workspace (and synchronises the stream).  With a comm: one allreduce of all
- * vectors' active parts.  Errors: INVALID_ARGUMENT, ALIAS, CUDA, NCCL, OUT_OF_MEMORY. */
+ * Two strategies, chosen by the plan's STTSV_BATCH_FUSED flag:
+ *  - default: one sttsv_apply pass per vector (the edge stream is re-read per
+ *    vector).  On B200 the single-vector edge kernel is issue/FP64-bound, not
+ *    HBM-bound, so this is the faster one on every measured
+ *    configuration; any plan, including STTSV_DETERMINISTIC.
+ *  - STTSV_BATCH_FUSED: the hyperedge stream is read ONCE for all vectors; each
+ *    vector's DP and scatter run in turn on the staged tile (per-tile run
+ *    flushes).  Pays only where the single pass is HBM-bound.  The first call
+ *    with a larger nvec allocates a workspace (and synchronises the stream);
+ *    with a comm, one allreduce of all vectors' active parts; not with
+ *    STTSV_DETERMINISTIC and nvec > 1 (UNSUPPORTED).
+ * Stream-ordered like sttsv_apply.  Errors: INVALID_ARGUMENT, ALIAS, UNSUPPORTED,
+ * CUDA, NCCL, OUT_OF_MEMORY. */
 #define STTSV_MAX_BATCH 16
 sttsv_status_t sttsv_apply_batch(sttsv_plan_t plan, const double* X_dev, double* Y_dev, int nvec, int64_t ld,
                                  void* stream);

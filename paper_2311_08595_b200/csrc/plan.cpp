@@ -233,6 +233,7 @@ struct sttsv_plan_s {
   double* h_xa = nullptr;      // pinned staging of x on the active vertices
   // deterministic mode (STTSV_DETERMINISTIC): slot pool, vertex-major buffer, chunks
   bool det = false;
+  bool batch_fused = false;  // STTSV_BATCH_FUSED: sttsv_apply_batch as one pass over the edge stream
   void* det_mem = nullptr;
   int64_t det_chunks = 0;
   double *d_contrib = nullptr, *d_csum = nullptr;
@@ -339,7 +340,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (world < 1 || rank < 0 || rank >= world) return fail(STTSV_ERR_INVALID_ARGUMENT, "bad world/rank");
   if (comm && (comm->world != world || comm->rank != rank || comm->device != device))
     return fail(STTSV_ERR_INVALID_ARGUMENT, "comm world/rank/device differ from the plan's");
-  const uint32_t known = STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES | STTSV_DETERMINISTIC;
+  const uint32_t known = STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES | STTSV_DETERMINISTIC | STTSV_BATCH_FUSED;
   if (flags & ~known) return fail(STTSV_ERR_UNSUPPORTED, "flags 0x%x not implemented in this build", flags & ~known);
 
   // ---- validate; offsets
@@ -580,6 +581,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<int32_t> h_slot;
   std::vector<int64_t> h_cstart, h_vchunk;
   int64_t det_total = 0;
+  p->batch_fused = (flags & STTSV_BATCH_FUSED) != 0;
   if (flags & STTSV_DETERMINISTIC) {
     p->det = true;
     std::vector<int64_t> voff(na + 1, 0);
@@ -965,13 +967,23 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
   if (!p || !X || !Y) return fail(STTSV_ERR_INVALID_ARGUMENT, "NULL argument");
   if (nvec < 1 || nvec > STTSV_MAX_BATCH) return fail(STTSV_ERR_INVALID_ARGUMENT, "nvec must be in [1, %d]", STTSV_MAX_BATCH);
   if (ld < p->n) return fail(STTSV_ERR_INVALID_ARGUMENT, "ld < n");
-  if (p->det && nvec > 1) return fail(STTSV_ERR_UNSUPPORTED, "batched apply of a STTSV_DETERMINISTIC plan");
+  if (p->batch_fused && p->det && nvec > 1)
+    return fail(STTSV_ERR_UNSUPPORTED, "fused batched apply of a STTSV_DETERMINISTIC plan");
   const size_t span = ((size_t)(nvec - 1) * (size_t)ld + (size_t)p->n) * sizeof(double);
   if (overlap(X, span, Y, span)) return fail(STTSV_ERR_ALIAS, "X and Y overlap");
   DeviceGuard g(p->device);
   sttsv_status_t st = check_async(p);
   if (st != STTSV_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!p->batch_fused) {
+    // one single-vector pass per vector (faster on B200 while the single pass is
+    // issue-bound; X and Y do not overlap)
+    for (int v = 0; v < nvec; ++v) {
+      st = apply_dense(p, X + (size_t)v * ld, Y + (size_t)v * ld, s);
+      if (st != STTSV_OK) return st;
+    }
+    return STTSV_OK;
+  }
   const int64_t na = p->n_active;
   if (p->batch_cap < nvec) {
     CUDA_TRY(cudaStreamSynchronize(s), "synchronize");

@@ -21,6 +21,7 @@ MAX_RANK = 32
 STTSV_CANONICALIZE = 1 << 0
 STTSV_MERGE_DUPLICATES = 1 << 1
 STTSV_DETERMINISTIC = 1 << 2
+STTSV_BATCH_FUSED = 1 << 3
 
 STATUS = {0: "STTSV_OK", 1: "STTSV_ERR_INVALID_ARGUMENT", 2: "STTSV_ERR_EDGE_SIZE", 3: "STTSV_ERR_VERTEX_RANGE",
           4: "STTSV_ERR_UNSORTED", 5: "STTSV_ERR_REPEATED_VERTEX", 6: "STTSV_ERR_NONFINITE", 7: "STTSV_ERR_ALIAS",

@@ -294,14 +294,16 @@ def test_hec_matches_oracle(S, torch_cuda):
     plan.close()
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("name,m,n,nvec", [("tiny", None, None, 3), ("mid", 100_000, None, 4),
                                            ("large", 200_000, 1_000_000, 2), ("high-rank", 800, None, 3),
                                            ("centrality", 50_000, None, 5)])
-def test_apply_batch(S, torch_cuda, name, m, n, nvec):
-    """f4: Y_v = B X_v^{N-1} for several vectors sharing one pass over the edge stream."""
+def test_apply_batch(S, torch_cuda, name, m, n, nvec, fused):
+    """f4: Y_v = B X_v^{N-1} for several vectors: one fused pass over the edge stream
+    (STTSV_BATCH_FUSED) or one single-vector pass per vector (default)."""
     torch = torch_cuda
     hg = W.generate(name, m=m, n=n)
-    plan = S.Plan.from_hypergraph(hg)
+    plan = S.Plan.from_hypergraph(hg, flags=S.STTSV_BATCH_FUSED if fused else 0)
     rng = np.random.default_rng(nvec)
     ld = hg.n + 7                                   # padded rows
     Xh = rng.uniform(0.05, 1.0, size=(nvec, ld))
@@ -332,7 +334,15 @@ def test_deterministic(S, torch_cuda, name, m, n):
     # a second plan built from the same input gives the same bits
     y2 = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC).apply(x).cpu().numpy()
     assert np.array_equal(y2.view(np.int64), ys[0].view(np.int64))
+    # the default batched apply (one pass per vector) keeps the bits
+    Y = plan.apply_batch(torch.stack([x, x])).cpu().numpy()
+    for v in range(2):
+        assert np.array_equal(Y[v].view(np.int64), ys[0].view(np.int64))
     plan.close()
+    fplan = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC | S.STTSV_BATCH_FUSED)
+    with pytest.raises(S.SttsvError, match="UNSUPPORTED"):
+        fplan.apply_batch(torch.stack([x, x]))
+    fplan.close()
 
 
 # ------------------------------------------------ scatter tiers (SURVEY.md §4 layer 2)
@@ -410,7 +420,7 @@ def test_fuzz(S, torch_cuda, seed):
         y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
     elif mode == 1:
         y = plan.apply_host(hg.x)
-    elif mode == 2 and flags != S.STTSV_DETERMINISTIC:
+    elif mode == 2:
         X = torch.from_numpy(np.stack([hg.x, 0.5 * hg.x])).cuda()
         Y = plan.apply_batch(X).cpu().numpy()
         assert rel(Y[1], 0.5 ** (N - 1) * ref) < TOL     # homogeneity
@@ -430,7 +440,7 @@ def test_interleaved_entry_points(S, torch_cuda, name, m, n):
     call must see all tiles exactly once."""
     torch = torch_cuda
     hg = W.generate(name, m=m, n=n)
-    plan = S.Plan.from_hypergraph(hg)
+    plan = S.Plan.from_hypergraph(hg, flags=S.STTSV_BATCH_FUSED if name != "mid" else 0)
     ref = oracle.sttsv(hg)
     x = torch.from_numpy(hg.x).cuda()
     rng = np.random.default_rng(7)

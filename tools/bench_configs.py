@@ -76,7 +76,7 @@ def main():
                "edge_kernel_fp64_frac": 2 * info["fma_per_apply"] / (kavg * 1e-3) / 1e12 / fp64,
                "alg_bytes": alg_bytes, "fma_per_apply": info["fma_per_apply"],
                "peaks": {"hbm_gbs": hbm, "hbm_src": hbm_src, "fp64_tflops": fp64, "fp64_src": fp64_src}}
-        # f4: 4 vectors per pass over the edge stream
+        # f4: 4 vectors, one pass per vector (default) and one fused pass (STTSV_BATCH_FUSED)
         X = x.unsqueeze(0).repeat(4, 1)
         Y = torch.empty_like(X)
         plan.apply_batch(X, Y)
@@ -84,7 +84,13 @@ def main():
         bmed, _ = ev_time(lambda: plan.apply_batch(X, Y), args.reps, stream)
         rec["batch4_ms"] = bmed
         rec["batch4_vector_incidences_per_s"] = 4 * hg.incidences / (bmed * 1e-3)
-        del X, Y
+        fplan = S.Plan.from_hypergraph(hg, flags=S.STTSV_BATCH_FUSED)
+        fplan.apply_batch(X, Y)
+        torch.cuda.synchronize()
+        fmed, _ = ev_time(lambda: fplan.apply_batch(X, Y), args.reps, stream)
+        rec["batch4_fused_ms"] = fmed
+        fplan.close()
+        del fplan, X, Y
         # f2: deterministic plan (vertex-major stores + fixed-order sums)
         dplan = S.Plan.from_hypergraph(hg, flags=S.STTSV_DETERMINISTIC)
         for _ in range(3):
