@@ -268,7 +268,10 @@ def run_ours(args):
                      "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
 
     # ---------------- roofline of the dominant kernel (edge kernel)
+    # algorithmic bytes per SURVEY.md 8(d): the int32-id / fp64-weight store; the
+    # plan may stream the ids as uint16 (n_active <= 65536), reported separately
     alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
+    phys_bytes = info["id_bytes"] * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
     fp64_peak, fp64_src = fp64_peak_tflops()
@@ -277,7 +280,13 @@ def run_ours(args):
                 "traffic": ncu_traffic(args.config), "kernel": "sttsv::edge_kernel<N>",
                 "kernel_ms": kern_avg, "kernel_share_of_step": kern_avg / ms_step,
                 "alg_bytes_per_launch": alg_bytes,
-                "alg_bytes_def": "4*sum|e| (int32 ids) + 8*m (fp64 w') + 8*n_active (x_a) + 8*n_active (y_a) per shard",
+                "alg_bytes_def": "SURVEY.md 8(d), int32/fp64 store: 4*sum|e| (ids) + 8*m (fp64 w') + 8*n_active (x_a) "
+                                 "+ 8*n_active (y_a) per shard",
+                "stream": {"id_bytes": info["id_bytes"], "bytes_per_launch": phys_bytes,
+                           "gbs": phys_bytes / (kern_avg * 1e-3) / 1e9,
+                           "frac": phys_bytes / (kern_avg * 1e-3) / 1e9 / peak,
+                           "note": "bytes the kernel actually streams: member ids as uint16 when n_active <= 65536 "
+                                   "(every relabelled id fits); compare with traffic"},
                 "peak_source": peak_src,
                 "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_tf / fp64_peak,
                          "peak_source": fp64_src,

@@ -198,9 +198,11 @@ typedef struct {
   int64_t stream_bytes;    /* bytes of the edge stream one apply reads (ids + weights, incl. tile padding) */
   double  fma_per_apply;   /* FP64 fused multiply-adds of the per-edge DP per apply      */
   int32_t hot_private;     /* slots 0..T-1 of every edge accumulate in per-lane register runs */
-  int32_t hot_shared;      /* H: ids below H accumulate in CTA shared memory            */
+  int32_t hot_shared;      /* H: ids below H accumulate in per-CTA L2 slices            */
   int32_t kernel_grid;     /* CTAs of the edge kernel                                    */
   int32_t kernel_block;    /* threads per CTA of the edge kernel                         */
+  int32_t id_bytes;        /* bytes per member id in the edge stream: 2 when n_active <= 65536
+                              on ranks <= 12, else 4                                      */
 } sttsv_plan_info_t;
 
 sttsv_status_t sttsv_plan_info(sttsv_plan_t plan, sttsv_plan_info_t* info);

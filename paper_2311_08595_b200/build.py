@@ -30,6 +30,12 @@ def compiled_ranks() -> list[int]:
     return [int(v) for v in re.findall(r"X\((\d+)\)", m.group(1))]
 
 
+def id16_ranks() -> list[int]:
+    src = open(os.path.join(CSRC, "internal.h")).read()
+    m = re.search(r"#define STTSV_ID16_RANKS\(X\)\s*\\\s*\n(.*)\n", src)
+    return [int(v) for v in re.findall(r"X\((\d+)\)", m.group(1))]
+
+
 def _newest_dep() -> float:
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "sttsv.h")]
     return max(os.path.getmtime(d) for d in deps)
@@ -50,6 +56,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     for n in compiled_ranks() + [0]:
         units.append((os.path.join(OBJ, "edge_n%d.o" % n),
                       [NVCC] + NVFLAGS + ["-DSTTSV_INST_N=%d" % n, "-c", os.path.join(CSRC, "edge_inst.cu")]))
+    for n in id16_ranks():
+        units.append((os.path.join(OBJ, "edge16_n%d.o" % n),
+                      [NVCC] + NVFLAGS + ["-DSTTSV_INST_N=%d" % n, "-DSTTSV_INST_ID16=1", "-c",
+                                          os.path.join(CSRC, "edge_inst.cu")]))
     units.append((os.path.join(OBJ, "kernels.o"), [NVCC] + NVFLAGS + ["-c", os.path.join(CSRC, "kernels.cu")]))
     units.append((os.path.join(OBJ, "plan.o"),
                   [NVCC] + NVFLAGS + ["-Xcompiler", "-fopenmp", "-c", os.path.join(CSRC, "plan.cpp")]))

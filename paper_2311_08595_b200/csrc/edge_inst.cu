@@ -10,22 +10,34 @@
 #define STTSV_CAT2(a, b) a##b
 #define STTSV_CAT(a, b) STTSV_CAT2(a, b)
 
+// -DSTTSV_INST_ID16=1: the 16-bit-id instantiation (edge_entry16_<N>, STTSV_ID16_RANKS)
+#ifndef STTSV_INST_ID16
+#define STTSV_INST_ID16 0
+#endif
+
 namespace sttsv {
+#if STTSV_INST_ID16
+EdgeKernelEntry STTSV_CAT(edge_entry16_, STTSV_INST_N)() {
+  constexpr int IDB = 2;
+#else
 EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
+  constexpr int IDB = 4;
+#endif
+  using C = EdgeCfg<STTSV_INST_N, IDB>;
   EdgeKernelEntry e;
-  e.fn = (const void*)edge_kernel<STTSV_INST_N, false, false>;
-  e.fn_batch = (const void*)edge_kernel<STTSV_INST_N, true, false>;
-  e.fn_det = (const void*)edge_kernel<STTSV_INST_N, false, true>;
-  e.block = EdgeCfg<STTSV_INST_N>::THREADS;
-  e.tile = EdgeCfg<STTSV_INST_N>::TILE;
-  e.ring_bytes = (size_t)EdgeCfg<STTSV_INST_N>::RING_BYTES;
+  e.fn = (const void*)edge_kernel<STTSV_INST_N, false, false, IDB>;
+  e.fn_batch = (const void*)edge_kernel<STTSV_INST_N, true, false, IDB>;
+  e.fn_det = (const void*)edge_kernel<STTSV_INST_N, false, true, IDB>;
+  e.block = C::THREADS;
+  e.tile = C::TILE;
+  e.ring_bytes = (size_t)C::RING_BYTES;
   e.rank = STTSV_INST_N;
-  e.run_slots = EdgeCfg<STTSV_INST_N>::RMAX;
-  e.big = EdgeCfg<STTSV_INST_N>::BIG ? (STTSV_BIG_LOCAL ? 2 : 1) : 0;
-  e.consumers = 32 * EdgeCfg<STTSV_INST_N>::NCW;
-  e.epl = EdgeCfg<STTSV_INST_N>::EPL;
-  e.table_norm = ((EdgeCfg<STTSV_INST_N>::BIG && STTSV_BIG_NORM) ||
-                  (!EdgeCfg<STTSV_INST_N>::BIG && STTSV_INST_N >= STTSV_NORM_MIN && STTSV_MID_NORM)) ? 1 : 0;
+  e.run_slots = C::RMAX;
+  e.big = C::BIG ? (STTSV_BIG_LOCAL ? 2 : 1) : 0;
+  e.consumers = 32 * C::NCW;
+  e.epl = C::EPL;
+  e.id_bytes = C::IDB;
+  e.table_norm = ((C::BIG && STTSV_BIG_NORM) || (!C::BIG && STTSV_INST_N >= STTSV_NORM_MIN && STTSV_MID_NORM)) ? 1 : 0;
   return e;
 }
 }  // namespace sttsv

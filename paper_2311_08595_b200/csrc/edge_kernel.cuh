@@ -41,6 +41,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "dp.cuh"
 #include "internal.h"
 
@@ -114,12 +116,15 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #define STTSV_WAIT_HINT_NS 1000000
 #endif
 
-template <int N>
+// IDB_: bytes per member id in the edge stream (4; or 2 for plans with n_a <=
+// 65536 on the unrolled ranks: 36% fewer stream bytes at mean k = 5)
+template <int N, int IDB_ = 4>
 struct EdgeCfg {
   static constexpr bool BIG = (N == 0) || (N >= STTSV_BIG_MIN);
   static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
   static constexpr int EPL = BIG ? 1 : STTSV_EPL;           // consecutive edges per lane per tile (odd)
-  static constexpr int EDGE_BYTES = 4 * KMAX + 8;           // staged bytes per edge (ids + w')
+  static constexpr int IDB = BIG ? 4 : IDB_;               // bytes per member id in the stream
+  static constexpr int EDGE_BYTES = IDB * KMAX + 8;         // staged bytes per edge (ids + w')
   // dynamic shared memory for the TMA ring (<= 227 KB in total; the large-rank
   // path also needs its prefix stack)
   static constexpr int RING_BUDGET =
@@ -127,7 +132,8 @@ struct EdgeCfg {
   // consumer warps per CTA (NCW_PREF), fewer when two stages of the largest
   // bucket would not fit the ring budget
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
-  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW) : (N <= 8 ? STTSV_NCW_SMALL : N <= 10 ? STTSV_NCW_SMALL9 : STTSV_NCW_MID);
+  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW)
+                                      : (N <= 8 ? STTSV_NCW_SMALL : N <= 10 ? STTSV_NCW_SMALL9 : STTSV_NCW_MID);
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
@@ -286,8 +292,8 @@ __device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (
 // The warp's block of a staged tile (size-K bucket): lane l takes the EPL
 // consecutive columns base + l*EPL + r, r = 0..EPL-1.  Buckets are padded to
 // whole tiles with weight-0 copies of their last edge, so every column is valid.
-template <int N, int K, int TILE, int EPL, int RMAX, bool DET>
-__device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, const double* __restrict__ sw, int base,
+template <int N, int K, int TILE, int EPL, int RMAX, bool DET, typename IdT>
+__device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const double* __restrict__ sw, int base,
                                            const double* __restrict__ xg, RunAcc<RMAX>& ra, const Sink& sk,
                                            const DetSink& ds, int lane) {
   constexpr int L = N - K + 1;
@@ -300,7 +306,7 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
     const double* rows[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      id[i] = sids[i * TILE + col];
+      id[i] = (int)sids[i * TILE + col];
       rows[i] = xg + (size_t)(uint32_t)id[i] * GS;  // GS compile-time: one IMAD.WIDE.U32
     }
     const double w = sw[col];
@@ -320,16 +326,16 @@ __device__ __forceinline__ void warp_block(const int32_t* __restrict__ sids, con
   }
 }
 
-template <int N, int K, int TILE, int EPL, int RMAX, bool DET>
-__device__ __forceinline__ void dispatch_k(int k, const int32_t* sids, const double* sw, int base,
+template <int N, int K, int TILE, int EPL, int RMAX, bool DET, typename IdT>
+__device__ __forceinline__ void dispatch_k(int k, const IdT* sids, const double* sw, int base,
                                            const double* xg, RunAcc<RMAX>& ra, const Sink& sk, const DetSink& ds,
                                            int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      warp_block<N, K, TILE, EPL, RMAX, DET>(sids, sw, base, xg, ra, sk, ds, lane);
+      warp_block<N, K, TILE, EPL, RMAX, DET, IdT>(sids, sw, base, xg, ra, sk, ds, lane);
       return;
     }
-    dispatch_k<N, K + 1, TILE, EPL, RMAX, DET>(k, sids, sw, base, xg, ra, sk, ds, lane);
+    dispatch_k<N, K + 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xg, ra, sk, ds, lane);
   }
 }
 
@@ -588,10 +594,11 @@ __device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid
 // BATCH = false: one vector (sttsv_apply; runs continue across tiles);
 // BATCH = true: p.nvec vectors per tile (sttsv_apply_batch, f4).
 // DET = true: deterministic stores into the vertex-major buffer (f2; one vector).
-template <int N, bool BATCH, bool DET>
-__global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
+// IDB: bytes per member id in the edge stream (EdgeCfg).
+template <int N, bool BATCH, bool DET, int IDB = 4>
+__global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN_BLOCKS)
     edge_kernel(const __grid_constant__ EdgeKernelParams p) {
-  using Cfg = EdgeCfg<N>;
+  using Cfg = EdgeCfg<N, IDB>;
   constexpr int TILE = Cfg::TILE, KMAX = Cfg::KMAX, NCW = Cfg::NCW, EPL = Cfg::EPL;
   constexpr int RMAX = Cfg::RMAX;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         if (t >= 0)
           while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const int k = t >= 0 ? p.b[b].k : 0;
-        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (4 * k + 8)) : 0u;
+        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (Cfg::IDB * k + 8)) : 0u;
         uint64_t start = head;
         if (start % Cfg::RING_BYTES + need > (uint64_t)Cfg::RING_BYTES) start += Cfg::RING_BYTES - start % Cfg::RING_BYTES;
         while (it - oldest >= SLOTS || (oldest < it && start + need - tail > (uint64_t)Cfg::RING_BYTES)) {
@@ -663,12 +670,13 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
         }
         const BucketDesc& bd = p.b[b];
         const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
-        constexpr uint32_t id_bytes = TILE * 4, w_bytes = TILE * 8;
+        constexpr uint32_t id_bytes = TILE * Cfg::IDB, w_bytes = TILE * 8;
         unsigned char* st = ring + off;
+        const unsigned char* idp = reinterpret_cast<const unsigned char*>(p.ids);
         mbar_arrive_expect_tx(&full[s], need);
         for (int i = 0; i < k; ++i)
-          bulk_g2s(st + i * TILE * 4, p.ids + bd.ids_off + i * bd.stride + e0, id_bytes, &full[s]);
-        bulk_g2s(st + k * TILE * 4, p.w + bd.w_off + e0, w_bytes, &full[s]);
+          bulk_g2s(st + i * id_bytes, idp + (size_t)(bd.ids_off + i * bd.stride + e0) * Cfg::IDB, id_bytes, &full[s]);
+        bulk_g2s(st + k * id_bytes, p.w + bd.w_off + e0, w_bytes, &full[s]);
       }
     }
   } else {
@@ -713,15 +721,16 @@ __global__ void __launch_bounds__(EdgeCfg<N>::THREADS, EdgeCfg<N>::MIN_BLOCKS)
                        p.contrib};
       {
         const unsigned char* st = ring + soff[s];
-        const int32_t* sids = reinterpret_cast<const int32_t*>(st);
-        const double* sw = reinterpret_cast<const double*>(st + k * TILE * 4);
+        using IdT = typename std::conditional<Cfg::IDB == 2, uint16_t, int32_t>::type;
+        const IdT* sids = reinterpret_cast<const IdT*>(st);
+        const double* sw = reinterpret_cast<const double*>(st + k * TILE * Cfg::IDB);
         // one pass per vector; with several vectors the runs of a pass are flushed
         // (warp-aggregated) at its end, with one they continue across tiles
         for (int v = 0; v < nvec; ++v) {
           const Sink skv{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H};
           const double* xgv = p.xg + (size_t)v * p.xg_vstride;
           if constexpr (!Cfg::BIG) {
-            dispatch_k<N, 1, TILE, EPL, RMAX, DET>(k, sids, sw, base, xgv, ra, skv, ds, lane);
+            dispatch_k<N, 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xgv, ra, skv, ds, lane);
           } else {
             const int col = warp * 32 + lane;  // EPL = 1
 #if STTSV_BIG_LOCAL

@@ -76,14 +76,24 @@ struct EdgeKernelEntry {
   int consumers;       // consumer threads per CTA
   int table_norm;      // series table rows normalised to a leading 1 (dp.cuh series_row norm = 1)
   int epl;             // consecutive edges per lane per tile (lane l: columns l*epl .. l*epl+epl-1 of its warp block)
+  int id_bytes;        // bytes per member id in the edge stream (4, or 2: plans with n_a <= 65536)
 };
+// Ranks that also have a 16-bit-member-id instantiation (unrolled path; used by
+// plans with n_a <= 65536).
+#define STTSV_ID16_RANKS(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
+
 #define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry_##n();
 STTSV_COMPILED_RANKS(STTSV_DECLARE_ENTRY)
+#undef STTSV_DECLARE_ENTRY
+#define STTSV_DECLARE_ENTRY(n) EdgeKernelEntry edge_entry16_##n();
+STTSV_ID16_RANKS(STTSV_DECLARE_ENTRY)
 EdgeKernelEntry edge_entry_0();
 #undef STTSV_DECLARE_ENTRY
 
 // launchers (kernels.cu)
-EdgeKernelEntry edge_entry(int N);
+// id16: prefer the 16-bit-id instantiation (falls back to 32-bit ids where none exists)
+EdgeKernelEntry edge_entry(int N, bool id16 = false);
 // dynamic shared memory of the edge kernel for rank N (TMA ring + large-rank prefix stacks)
 size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N);
 // doubles of prefix stack per consumer thread of the large-rank path (edge_kernel.cuh)

@@ -231,7 +231,18 @@ __global__ void __launch_bounds__(kDetBlock) det_vertex_kernel(const double* __r
 }
 
 // ------------------------------------------------------------- launchers
-EdgeKernelEntry edge_entry(int N) {
+EdgeKernelEntry edge_entry(int N, bool id16) {
+  if (id16) {
+    switch (N) {
+#define STTSV_CASE(n) \
+  case n:             \
+    return edge_entry16_##n();
+      STTSV_ID16_RANKS(STTSV_CASE)
+#undef STTSV_CASE
+      default:
+        break;
+    }
+  }
   switch (N) {
 #define STTSV_CASE(n) \
   case n:             \

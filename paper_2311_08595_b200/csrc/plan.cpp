@@ -410,8 +410,11 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   // ---- buckets and this shard's slices
   std::vector<int64_t> pos, count;
   bucket_positions(m, sizes, N, pos, count);
-  p->ent = edge_entry(N);
+  // 16-bit member ids in the edge stream when every relabelled id fits
+  // (STTSV_ID32=1 forces 32-bit ids, for experiments)
+  p->ent = edge_entry(N, na <= 65536 && !getenv("STTSV_ID32"));
   const int tile = p->ent.tile;
+  const int idb = p->ent.id_bytes;  // 2: 16-bit member ids in the edge stream
   std::vector<int64_t> lo(N + 1), mk(N + 1, 0), stride(N + 1, 0);
   for (int k = 1; k <= N; ++k) {
     lo[k] = bucket_lo(count[k], world, rank);
@@ -552,7 +555,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     fma += dp_fma(N, k) * (double)stored[k];
     p->stored_edges += stored[k];
     p->stored_inc += stored[k] * k;
-    p->stream_bytes += (stored[k] + tile - 1) / tile * tile * (4 * k + 8);
+    p->stream_bytes += (stored[k] + tile - 1) / tile * tile * (idb * k + 8);
   }
   kp.num_tiles = tiles;
   kp.n_active = (int32_t)na;
@@ -626,7 +629,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   // ---- device memory: one allocation
   DeviceGuard g(device);
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t b_ids = align(ids_total * 4), b_w = align(w_total * 8), b_act = align(na * 4 + 4),
+  const size_t b_ids = align(ids_total * idb), b_w = align(w_total * 8), b_act = align(na * 4 + 4),
                b_xa = align(na * 8 + 8), b_ya = align(na * 8 + 8), b_scr = align((2 * kNormalizeScratch + 4) * 8);
   const int gs = series_stride(N);
   const size_t b_xg = align((size_t)na * gs * 8 + 16);
@@ -646,7 +649,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   unsigned long long* d_cnt = (unsigned long long*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg);
   double* d_priv = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta);
   p->gs = gs;
-  if (ids_total) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
+  if (ids_total && idb == 4) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
+  if (ids_total && idb == 2) {
+    std::vector<uint16_t> h16((size_t)ids_total);
+    for (int64_t i = 0; i < ids_total; ++i) h16[i] = (uint16_t)h_ids[i];
+    ce = cudaMemcpy(d_ids, h16.data(), ids_total * 2, cudaMemcpyHostToDevice);
+  }
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
   p->h_act = act;
@@ -712,6 +720,7 @@ extern "C" sttsv_status_t sttsv_plan_info(sttsv_plan_t p, sttsv_plan_info_t* inf
   info->hot_shared = p->kp.H;
   info->kernel_grid = p->grid;
   info->kernel_block = p->block;
+  info->id_bytes = p->ent.id_bytes;
   return STTSV_OK;
 }
 

@@ -43,7 +43,8 @@ class PlanInfo(ctypes.Structure):
                 ("n_active", ctypes.c_int64), ("edges_per_size", ctypes.c_int64 * (MAX_RANK + 1)),
                 ("device_bytes", ctypes.c_int64), ("stream_bytes", ctypes.c_int64),
                 ("fma_per_apply", ctypes.c_double), ("hot_private", ctypes.c_int32),
-                ("hot_shared", ctypes.c_int32), ("kernel_grid", ctypes.c_int32), ("kernel_block", ctypes.c_int32)]
+                ("hot_shared", ctypes.c_int32), ("kernel_grid", ctypes.c_int32), ("kernel_block", ctypes.c_int32),
+                ("id_bytes", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "edges_per_size"}

@@ -498,3 +498,27 @@ def test_apply_in_cuda_graph(S, torch_cuda):
         for i in range(3):
             assert rel(ys[i].cpu().numpy(), oracle.sttsv(hg, x=xs[i])) < TOL, (rep, i)
     plan.close()
+
+
+@pytest.mark.parametrize("name,m,n", [("mid", 200_000, None), ("large", 300_000, 2_000_000), ("centrality", 100_000, None)])
+def test_id_width(S, torch_cuda, name, m, n, monkeypatch):
+    """The edge stream carries 16-bit member ids when n_active <= 65536 (ranks <= 12) and
+    32-bit ids otherwise (STTSV_ID32=1 forces them): both match the oracle."""
+    torch = torch_cuda
+    hg = W.generate(name, m=m, n=n)
+    ref = oracle.sttsv(hg)
+    x = torch.from_numpy(hg.x).cuda()
+    widths = {}
+    for force32 in (False, True):
+        if force32:
+            monkeypatch.setenv("STTSV_ID32", "1")
+        else:
+            monkeypatch.delenv("STTSV_ID32", raising=False)
+        plan = S.Plan.from_hypergraph(hg)
+        info = plan.info()
+        widths[force32] = info["id_bytes"]
+        assert info["stream_bytes"] >= info["id_bytes"] * info["incidences"] + 8 * info["num_edges"]
+        assert rel(plan.apply(x).cpu().numpy(), ref) < TOL, (name, force32)
+        plan.close()
+    expect16 = hg.rank <= 12 and int(np.count_nonzero(np.bincount(hg.indices, minlength=hg.n))) <= 65536
+    assert widths[True] == 4 and widths[False] == (2 if expect16 else 4)

@@ -65,7 +65,7 @@ def main():
         kms, kn = plan.profile_read()
         plan.profile(False)
         kavg = kms / max(kn, 1)
-        alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
+        alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]  # SURVEY 8(d)
         rec = {"config": name, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank, "incidences": hg.incidences,
                "n_active": info["n_active"], "plan_s": round(t_plan, 2),
                "apply_ms_median": med, "apply_ms_min": mn, "edge_kernel_ms": kavg,
@@ -74,7 +74,9 @@ def main():
                "edge_kernel_hbm_frac": alg_bytes / (kavg * 1e-3) / 1e9 / hbm,
                "edge_kernel_fp64_tflops": 2 * info["fma_per_apply"] / (kavg * 1e-3) / 1e12,
                "edge_kernel_fp64_frac": 2 * info["fma_per_apply"] / (kavg * 1e-3) / 1e12 / fp64,
-               "alg_bytes": alg_bytes, "fma_per_apply": info["fma_per_apply"],
+               "alg_bytes": alg_bytes, "fma_per_apply": info["fma_per_apply"], "id_bytes": info["id_bytes"],
+               "stream_hbm_frac": (info["id_bytes"] * info["incidences"] + 8 * info["num_edges"]
+                                   + 16 * info["n_active"]) / (kavg * 1e-3) / 1e9 / hbm,
                "peaks": {"hbm_gbs": hbm, "hbm_src": hbm_src, "fp64_tflops": fp64, "fp64_src": fp64_src}}
         # f4: 4 vectors, one pass per vector (default) and one fused pass (STTSV_BATCH_FUSED)
         X = x.unsqueeze(0).repeat(4, 1)

@@ -20,14 +20,18 @@ if not os.environ.get("VARIANTS_KEEP"):
     shutil.rmtree(out, ignore_errors=True)  # keep the gpurun snapshot small: only this call's variants
 os.makedirs(out, exist_ok=True)
 objs = [os.path.join(B.OBJ, "edge_n%d.o" % n) for n in B.compiled_ranks() + [0] if n != N]
+objs += [os.path.join(B.OBJ, "edge16_n%d.o" % n) for n in B.id16_ranks() if n != N]
 objs += [os.path.join(B.OBJ, "kernels.o"), os.path.join(B.OBJ, "plan.o")]
 for spec in sys.argv[2:]:
     name, _, flags = spec.partition(":")
     flags = [f for f in flags.split(",") if f]
-    o = os.path.join(out, "edge_n%d_%s.o" % (N, name))
-    subprocess.check_call([B.NVCC] + B.NVFLAGS + flags + ["-DSTTSV_INST_N=%d" % N, "-c",
-                           os.path.join(B.CSRC, "edge_inst.cu"), "-o", o])
+    vobjs = []
+    for id16 in ([0, 1] if N in B.id16_ranks() else [0]):
+        o = os.path.join(out, "edge%s_n%d_%s.o" % ("16" if id16 else "", N, name))
+        subprocess.check_call([B.NVCC] + B.NVFLAGS + flags + ["-DSTTSV_INST_N=%d" % N, "-DSTTSV_INST_ID16=%d" % id16,
+                               "-c", os.path.join(B.CSRC, "edge_inst.cu"), "-o", o])
+        vobjs.append(o)
     lib = os.path.join(out, "libsttsv_%s.so" % name)
-    subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib, o] + objs +
+    subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib] + vobjs + objs +
                           ["-ldl", "-lgomp"])
     print(lib)
