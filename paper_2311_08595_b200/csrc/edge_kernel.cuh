@@ -69,6 +69,10 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #ifndef STTSV_EPL
 #define STTSV_EPL 5
 #endif
+// edges per lane per tile with 16-bit member ids (smaller stages: more in flight)
+#ifndef STTSV_EPL16
+#define STTSV_EPL16 8
+#endif
 #ifndef STTSV_RING_KB
 #define STTSV_RING_KB 110
 #endif
@@ -122,8 +126,8 @@ template <int N, int IDB_ = 4>
 struct EdgeCfg {
   static constexpr bool BIG = (N == 0) || (N >= STTSV_BIG_MIN);
   static constexpr int KMAX = N < 1 ? STTSV_MAX_RANK : N;
-  static constexpr int EPL = BIG ? 1 : STTSV_EPL;           // consecutive edges per lane per tile (odd)
   static constexpr int IDB = BIG ? 4 : IDB_;               // bytes per member id in the stream
+  static constexpr int EPL = BIG ? 1 : (IDB == 2 ? STTSV_EPL16 : STTSV_EPL);  // consecutive edges per lane per tile
   static constexpr int EDGE_BYTES = IDB * KMAX + 8;         // staged bytes per edge (ids + w')
   // dynamic shared memory for the TMA ring (<= 227 KB in total; the large-rank
   // path also needs its prefix stack)
@@ -290,18 +294,19 @@ __device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (
 }
 
 // The warp's block of a staged tile (size-K bucket): lane l takes the EPL
-// consecutive columns base + l*EPL + r, r = 0..EPL-1.  Buckets are padded to
-// whole tiles with weight-0 copies of their last edge, so every column is valid.
+// consecutive sorted edges base + l*EPL + r, r = 0..EPL-1, which the plan
+// stores lane-major at columns base + r*32 + l (conflict-free shared reads).
+// Buckets are padded to whole tiles with weight-0 copies of their last edge,
+// so every column is valid.
 template <int N, int K, int TILE, int EPL, int RMAX, bool DET, typename IdT>
 __device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const double* __restrict__ sw, int base,
                                            const double* __restrict__ xg, RunAcc<RMAX>& ra, const Sink& sk,
                                            const DetSink& ds, int lane) {
   constexpr int L = N - K + 1;
   constexpr int GS = series_stride(N);
-  const int col0 = base + lane * EPL;
 #pragma unroll 1
   for (int r = 0; r < EPL; ++r) {
-    const int col = col0 + r;
+    const int col = base + r * 32 + lane;  // lane-major tile layout (plan.cpp): sorted edge base + lane*EPL + r
     int id[K];
     const double* rows[K];
 #pragma unroll

@@ -626,6 +626,37 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     h_cstart.push_back(det_total);
   }
 
+  // ---- lane-major tile layout: within each warp block of 32*epl columns, lane l
+  // walks the epl CONSECUTIVE sorted edges l*epl + r (its register runs follow
+  // the sort order), stored at column r*32 + l so that a warp's read of one
+  // member slot at step r touches 32 consecutive ids (bank-conflict-free for
+  // 2- and 4-byte ids).  Ids, weights and the deterministic slot pool move alike.
+  if (p->ent.epl > 1) {
+    const int epl = p->ent.epl, wblock = 32 * epl;
+    for (int i = 0; i < kp.nb; ++i) {
+      const BucketDesc& bd = kp.b[i];
+      const int64_t cols = (bd.m + tile - 1) / tile * tile;  // whole tiles (a tile is whole warp blocks)
+      auto permute = [&](auto* base) {
+        using T = std::remove_reference_t<decltype(*base)>;
+#pragma omp parallel
+        {
+          std::vector<T> tmp(wblock);
+#pragma omp for schedule(static)
+          for (int64_t b0 = 0; b0 < cols; b0 += wblock) {
+            for (int l = 0; l < 32; ++l)
+              for (int r = 0; r < epl; ++r) tmp[r * 32 + l] = base[b0 + l * epl + r];
+            std::copy(tmp.begin(), tmp.end(), base + b0);
+          }
+        }
+      };
+      for (int q = 0; q < bd.k; ++q) {
+        permute(h_ids.data() + bd.ids_off + q * bd.stride);
+        if (p->det) permute(h_slot.data() + bd.ids_off + q * bd.stride);
+      }
+      permute(h_w.data() + bd.w_off);
+    }
+  }
+
   // ---- device memory: one allocation
   DeviceGuard g(device);
   auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
