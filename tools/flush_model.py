@@ -19,7 +19,7 @@ relabel = np.empty(n, np.int64); relabel[order] = np.arange(n)
 ids = relabel[hg.indices].astype(np.int32)
 sizes = hg.sizes
 off = hg.offsets if hasattr(hg,'offsets') else None
-TILE, NCW, EPL, CH = 1280, 8, 5, 16
+TILE, NCW, EPL, CH = 2048, 8, 8, 10   # N = 8 with 16-bit ids (EdgeCfg), chunk as plan.cpp picks for large
 H = 256
 tot_red = 0; tot_inc = 0; tot_hot = 0
 start = 0
