@@ -64,7 +64,7 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 // ---- compile-time tuning (each default was chosen by A/B timing on B200 with
 // tools/variants.py + tools/time_apply.py)
 // small ranks (N <= 10): two CTAs per SM, each 8 (N <= 8) or 7 consumer warps + 1 producer
-// with a 110 KB ring (two independent TMA pipelines per SM measured 2.7% faster
+// with a 112 KB ring (two independent TMA pipelines per SM measured 2.7% faster
 // than one CTA of 15 consumers on `large`), 5 edges per lane per tile
 #ifndef STTSV_EPL
 #define STTSV_EPL 5
@@ -74,7 +74,7 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #define STTSV_EPL16 8
 #endif
 #ifndef STTSV_RING_KB
-#define STTSV_RING_KB 110
+#define STTSV_RING_KB 112
 #endif
 #ifndef STTSV_NCW_SMALL
 #define STTSV_NCW_SMALL 8
