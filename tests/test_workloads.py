@@ -4,21 +4,29 @@ import subprocess
 import sys
 
 import numpy as np
+import pytest
 
 import workloads as W
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_zipf_sampler_frequencies():
-    n, s, cnt = 1000, 2.0, 400_000
+@pytest.mark.parametrize("n,s", [(1000, 2.0), (50, 2.2), (10_000_000, 2.2), (200, 1.5)])
+def test_zipf_sampler_frequencies(n, s):
+    """Devroye's rejection sampler conditioned on {1..n}: P(k) = k^-s / sum_{j<=n} j^-s."""
+    cnt = 400_000
     z = W.zipf_draws(3, n, s, cnt)
     assert z.min() >= 1 and z.max() <= n
-    p = np.arange(1, n + 1, dtype=np.float64) ** -s
-    p /= p.sum()
-    for r in (1, 2, 3, 5, 10):
+    p = np.arange(1, min(n, 10**6) + 1, dtype=np.float64) ** -s
+    p /= p.sum() + (0.0 if n <= 10**6 else (10**6) ** (1 - s) / (s - 1))   # tail of the normaliser (integral bound)
+    for r in (1, 2, 3, 5, 10, 40):
+        if r > n:
+            continue
         f = np.mean(z == r)
         assert abs(f - p[r - 1]) < 5 * np.sqrt(p[r - 1] / cnt) + 1e-4, (r, f, p[r - 1])
+    # tail mass beyond 40
+    if n > 40:
+        assert abs(np.mean(z > 40) - p[40:].sum()) < 5 * np.sqrt(p[40:].sum() / cnt) + 1e-4
 
 
 def test_iou_and_sizes():

@@ -52,36 +52,35 @@ static inline double rng_u01(rng_t* r) { return (double)(rng_next(r) >> 11) * 0x
 static inline double rng_u01_open0(rng_t* r) { return 1.0 - rng_u01(r); }
 
 /* ------------------------------------------ Zipf over {1..n}, exponent s -- */
-/* Rejection-inversion sampling (Hoermann & Derflinger 1996) restated for
- * P(k) proportional to k^-s, k = 1..n, s > 0.  hint(x) = integral of x^-s. */
+/* P(k) proportional to k^-s on {1..n}, s > 1 (every config draws members with
+ * s = 2.0 or 2.2).  The rejection method for the Zipf law in L. Devroye,
+ * "Non-Uniform Random Variate Generation" (Springer 1986), ch. X §6.1:
+ * propose X = floor(U^(-1/(s-1))) (a discretised Pareto variable), accept
+ * when V X (T - 1) / (b - 1) <= T / b with T = (1 + 1/X)^(s-1) and
+ * b = 2^(s-1).  That samples the unbounded law on {1, 2, ...}; proposals
+ * above n are rejected too, which conditions it on {1..n} (reading A9). */
 typedef struct {
-  double s, n, hint_x1, hint_n, sparam;
-} zipf_t;
+  double n;         /* upper end of the support */
+  double inv_sm1;   /* 1/(s-1) */
+  double sm1;       /* s-1 */
+  double b;         /* 2^(s-1) */
+} zipf_law;
 
-static double helper1(double x) { return fabs(x) > 1e-8 ? log1p(x) / x : 1.0 - x * (0.5 - x * (1.0 / 3.0 - 0.25 * x)); }
-static double helper2(double x) { return fabs(x) > 1e-8 ? expm1(x) / x : 1.0 + x * 0.5 * (1.0 + x * (1.0 / 3.0) * (1.0 + 0.25 * x)); }
-static double zh(const zipf_t* z, double x) { return exp(-z->s * log(x)); }
-static double zhint(const zipf_t* z, double x) { double lx = log(x); return helper2((1.0 - z->s) * lx) * lx; }
-static double zhint_inv(const zipf_t* z, double x) {
-  double t = x * (1.0 - z->s);
-  if (t < -1.0) t = -1.0;
-  return exp(helper1(t) * x);
-}
-static void zipf_init(zipf_t* z, int64_t n, double s) {
-  z->s = s;
+static void zipf_law_init(zipf_law* z, int64_t n, double s) {
   z->n = (double)n;
-  z->hint_x1 = zhint(z, 1.5) - 1.0;
-  z->hint_n = zhint(z, z->n + 0.5);
-  z->sparam = 2.0 - zhint_inv(z, zhint(z, 2.5) - zh(z, 2.0));
+  z->sm1 = s - 1.0;
+  z->inv_sm1 = 1.0 / (s - 1.0);
+  z->b = pow(2.0, s - 1.0);
 }
-static inline int64_t zipf_draw(const zipf_t* z, rng_t* r) {
+
+static inline int64_t zipf_law_draw(const zipf_law* z, rng_t* r) {
   for (;;) {
-    double u = z->hint_n + rng_u01(r) * (z->hint_x1 - z->hint_n);
-    double x = zhint_inv(z, u);
-    double kf = floor(x + 0.5);
-    if (kf < 1.0) kf = 1.0;
-    if (kf > z->n) kf = z->n;
-    if (kf - x <= z->sparam || u >= zhint(z, kf + 0.5) - zh(z, kf)) return (int64_t)kf;
+    const double u = rng_u01_open0(r); /* (0,1]: the power below stays finite */
+    const double v = rng_u01(r);
+    const double x = floor(z->sm1 == 1.0 ? 1.0 / u : pow(u, -z->inv_sm1));
+    if (x > z->n) continue;           /* outside {1..n}: condition by rejection */
+    const double t = z->sm1 == 1.0 ? 1.0 + 1.0 / x : pow(1.0 + 1.0 / x, z->sm1);
+    if (v * x * (t - 1.0) / (z->b - 1.0) <= t / z->b) return (int64_t)x;
   }
 }
 
@@ -133,8 +132,8 @@ static int cmp_i32(const void* a, const void* b) {
 int64_t gen_members(uint64_t seed, int64_t n, int64_t first, int64_t count,
                     const int32_t* sizes, const int64_t* offsets, int32_t kind,
                     double s, const int32_t* perm, int32_t* idx) {
-  zipf_t z;
-  if (kind == 1) zipf_init(&z, n, s);
+  zipf_law z;
+  if (kind == 1) zipf_law_init(&z, n, s);
   int64_t draws_total = 0;
 #pragma omp parallel for schedule(dynamic, 4096) reduction(+ : draws_total)
   for (int64_t i = 0; i < count; ++i) {
@@ -145,7 +144,7 @@ int64_t gen_members(uint64_t seed, int64_t n, int64_t first, int64_t count,
     while (have < k) {
       int32_t v;
       if (kind == 1) {
-        v = perm[zipf_draw(&z, &r) - 1];
+        v = perm[zipf_law_draw(&z, &r) - 1];
       } else {
         int64_t j = (int64_t)(rng_u01(&r) * (double)n);
         if (j >= n) j = n - 1;
@@ -198,8 +197,8 @@ void gen_uniform(uint64_t seed, uint64_t stream, int64_t count, double* out) {
 
 /* raw Zipf draws (tests of the generator) */
 void gen_zipf(uint64_t seed, int64_t n, double s, int64_t count, int64_t* out) {
-  zipf_t z;
-  zipf_init(&z, n, s);
+  zipf_law z;
+  zipf_law_init(&z, n, s);
   rng_t r = rng_at(seed, 6, 0);
-  for (int64_t i = 0; i < count; ++i) out[i] = zipf_draw(&z, &r);
+  for (int64_t i = 0; i < count; ++i) out[i] = zipf_law_draw(&z, &r);
 }
