@@ -151,7 +151,7 @@ def nqz(hg, tau: float, max_iters: int, rank=None, x0=None, nthreads: int = 0, h
     y = (1/n) 1 (line 3); z = TTSV1(y) (line 4); repeat { x = z^[1/(N-1)] / ||z^[1/(N-1)]||_1 (line 6);
     z = TTSV1(x) (line 7); lambda_min = min(z ./ x^[N-1]) (line 8); lambda_max = max(...) (line 9) }
     until (lambda_max - lambda_min)/lambda_min < tau (line 10) or max_iters repetitions.
-    min/max over vertices with x_v^(N-1) > 0 (reading A15 of DESIGN.md).  Returns (x, z, lambda_min, lambda_max, iters)
+    min/max over vertices with x_v > 0 (reading A15 of DESIGN.md).  Returns (x, z, lambda_min, lambda_max, iters)
     and, with history=True, also the list of (lambda_min, lambda_max) per repetition."""
     N = hg.rank if rank is None else int(rank)
     y = np.full(hg.n, 1.0 / hg.n) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
@@ -164,13 +164,13 @@ def nqz(hg, tau: float, max_iters: int, rank=None, x0=None, nthreads: int = 0, h
         r = np.power(z, 1.0 / (N - 1))
         x = r / r.sum()
         z = sttsv(hg, x=x, rank=N, nthreads=nthreads)
-        # x^[N-1] by repeated multiplication; vertices whose x^[N-1] is 0 (x = 0,
-        # or underflow) are excluded (reading A15 of DESIGN.md)
-        p = np.ones_like(x)
-        for _ in range(N - 1):
-            p = p * x
-        pos = p > 0
-        ratio = z[pos] / p[pos]
+        # lambda bracket of z ./ x^[N-1] (line 8-9) over the vertices with x_v > 0
+        # (reading A15 of DESIGN.md: isolated vertices have x = z = 0); the power
+        # and the ratio in long double (80-bit: x^(N-1) cannot underflow for any
+        # x_v > 1e-150 at N <= 32)
+        pos = x > 0
+        p = np.power(x[pos].astype(np.longdouble), N - 1)
+        ratio = z[pos].astype(np.longdouble) / p
         lo, hi = float(ratio.min()), float(ratio.max())
         hist.append((lo, hi))
         it += 1

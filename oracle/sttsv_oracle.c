@@ -104,50 +104,58 @@ static long double factorial_ld(int a) {
 typedef struct {
   int N, k;
   const double* xv;           /* x of the k members */
+  long double invx[ORACLE_MAX_RANK];  /* 1 / x_u (x_u != 0) */
   long double val;            /* w / |beta| */
   long double fact[ORACLE_MAX_RANK + 1];
-  long double pw[ORACLE_MAX_RANK][ORACLE_MAX_RANK + 1];   /* pw[u][t] = x_u^t */
+  long double pf[ORACLE_MAX_RANK][ORACLE_MAX_RANK + 1];   /* pf[u][t] = x_u^t / t! */
   int m[ORACLE_MAX_RANK];     /* current multiplicities */
   long double* out;
   long double* euler;         /* optional: accumulates sum over tuples of B_i prod x (all N factors) */
 } kappa_ctx;
 
-/* One multiset m in kappa(e): add the Eq. (2) terms of the tuples it groups. */
-static void kappa_visit(kappa_ctx* c) {
-  const int N = c->N, k = c->k;
+/* One multiset m in kappa(e), with T = prod_u x_u^{m_u} / m_u!: add the Eq. (2)
+ * terms of the ordered tuples it groups.  Of its N!/prod m_u! tuples,
+ * (N-1)!/((m_v-1)! prod_{u!=v} m_u!) start with v, and each adds
+ * w/|beta| * x_v^{m_v-1} prod_{u!=v} x_u^{m_u} to s_v; together that is
+ *     w/|beta| * (N-1)! * x_v^{m_v-1}/(m_v-1)! * prod_{u!=v} x_u^{m_u}/m_u!
+ *   = w/|beta| * (N-1)! * T * m_v / x_v                       (x_v != 0),
+ * the form written out in SURVEY.md §8(c).  For x_v = 0 only m_v = 1 survives
+ * (x_v^0 = 1) and the product over u != v is formed directly.  The factor
+ * w/|beta| * (N-1)!, common to every term of the edge, is applied once in
+ * kappa_edge (out[v] here accumulates T * m_v / x_v). */
+static void kappa_visit(kappa_ctx* c, long double T) {
+  const int k = c->k;
   for (int v = 0; v < k; ++v) {
-    /* number of ordered tuples with multiset m whose first entry is v */
-    long double count = c->fact[N - 1] / c->fact[c->m[v] - 1];
-    long double prod = 1.0L;      /* product of the other N-1 entries */
-    for (int u = 0; u < k; ++u) {
-      int mu = (u == v) ? c->m[u] - 1 : c->m[u];
-      if (u != v) count /= c->fact[c->m[u]];
-      prod *= c->pw[u][mu];
+    long double term;
+    if (c->xv[v] != 0.0) {
+      term = T * (long double)c->m[v] * c->invx[v];
+    } else if (c->m[v] == 1) {
+      long double prod = 1.0L;
+      for (int u = 0; u < k; ++u)
+        if (u != v) prod *= c->pf[u][c->m[u]];
+      term = prod;
+    } else {
+      term = 0.0L;
     }
-    c->out[v] += c->val * count * prod;
+    c->out[v] += term;
   }
-  if (c->euler) {
-    long double count = c->fact[N];
-    long double prod = 1.0L;
-    for (int u = 0; u < k; ++u) {
-      count /= c->fact[c->m[u]];
-      prod *= c->pw[u][c->m[u]];
-    }
-    *c->euler += c->val * count * prod;
-  }
+  /* Euler form: all N!/prod m_u! tuples, each val * prod_u x_u^{m_u} = N T per
+   * (N-1)! (the common factor applied in kappa_edge) */
+  if (c->euler) *c->euler += (long double)c->N * T;
 }
 
-/* enumerate compositions m_0..m_{k-1} >= 1 with sum N */
-static void kappa_rec(kappa_ctx* c, int pos, int remaining) {
+/* enumerate compositions m_0..m_{k-1} >= 1 with sum N; `part` carries
+ * prod_{u < pos} x_u^{m_u}/m_u! down the enumeration */
+static void kappa_rec(kappa_ctx* c, int pos, int remaining, long double part) {
   if (pos == c->k - 1) {
     c->m[pos] = remaining;
-    kappa_visit(c);
+    kappa_visit(c, part * c->pf[pos][remaining]);
     return;
   }
   int slots_after = c->k - 1 - pos;
   for (int mv = 1; mv <= remaining - slots_after; ++mv) {
     c->m[pos] = mv;
-    kappa_rec(c, pos + 1, remaining - mv);
+    kappa_rec(c, pos + 1, remaining - mv, part * c->pf[pos][mv]);
   }
 }
 
@@ -162,11 +170,21 @@ static void kappa_edge(int N, int k, const double* xv, long double val, long dou
   c.euler = euler;
   for (int i = 0; i <= N; ++i) c.fact[i] = factorial_ld(i);
   for (int u = 0; u < k; ++u) {
-    c.pw[u][0] = 1.0L;
-    for (int t = 1; t <= N; ++t) c.pw[u][t] = c.pw[u][t - 1] * (long double)xv[u];
+    long double pw = 1.0L;
+    c.invx[u] = xv[u] != 0.0 ? 1.0L / (long double)xv[u] : 0.0L;
+    c.pf[u][0] = 1.0L;
+    for (int t = 1; t <= N; ++t) {
+      pw *= (long double)xv[u];
+      c.pf[u][t] = pw / c.fact[t];
+    }
   }
   for (int i = 0; i < k; ++i) out[i] = 0.0L;
-  kappa_rec(&c, 0, N);
+  long double eu = 0.0L;
+  if (euler) c.euler = &eu;
+  kappa_rec(&c, 0, N, 1.0L);
+  const long double common = val * c.fact[N - 1];   /* w/|beta| * (N-1)! */
+  for (int i = 0; i < k; ++i) out[i] *= common;
+  if (euler) *euler += common * eu;
 }
 
 /* literal mode for one edge: all k^N maps positions -> members, surjective only */

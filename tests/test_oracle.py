@@ -311,3 +311,99 @@ def test_nqz_bracket_monotone_and_eigen_residual():
     assert (hi - lo) / lo < 1e-13 and it < 500
     lam = 0.5 * (lo + hi)
     assert rel_err(oracle.sttsv(hg, x=x), lam * x ** (N - 1)) < 1e-12
+
+
+# ------------------------------------------------ P13 per-bucket goldens ----
+def _surjections(N, k):
+    """|beta| = k! S(N,k) = number of surjections [N] -> [k] (inclusion-exclusion count)."""
+    return sum((-1) ** j * math.comb(k, j) * (k - j) ** N for j in range(k + 1))
+
+
+def _p13_exact(N, k, v):
+    """Exact s_v of the single edge {0..k-1}, x_i = 1/(i+2), w = 1.
+    k = N: P6 closed form (only permutations: (w/N) prod_{u != v} x_u);
+    otherwise P9, the subset expansion in exact rationals."""
+    x = [Fraction(1, i + 2) for i in range(k)]
+    if k == N:
+        p = Fraction(1, N)
+        for u in range(k):
+            if u != v:
+                p *= x[u]
+        return p
+    rest = [u for u in range(k) if u != v]
+    acc = Fraction(0)
+    for r in range(len(rest) + 1):
+        for T in itertools.combinations(rest, r):
+            acc += (-1) ** (k - 1 - r) * (x[v] + sum((x[u] for u in T), Fraction(0))) ** (N - 1)
+    return acc / _surjections(N, k)
+
+
+def test_p13_goldens_exact_and_oracle():
+    """the printed 17-digit values equal exact rationals computed here
+    (independently of the oracle), and the oracle reproduces them for every (N, k) row."""
+    g = json.load(open(os.path.join(GOLDEN, "p13.json")))
+    for c in g["cases"]:
+        N, k = c["N"], c["k"]
+        ex = {"y0": _p13_exact(N, k, 0), "y1": _p13_exact(N, k, 1), "ylast": _p13_exact(N, k, k - 1)}
+        for key, val in ex.items():
+            assert abs(float(val) - c[key]) <= 4.5e-16 * abs(c[key]), (N, k, key, float(val), c[key])   # 17 printed digits: <= 2 ulp
+        x = [1.0 / (i + 2) for i in range(k)]
+        y = oracle.sttsv(to_hg(k, N, [list(range(k))], [1.0], x))
+        for key, i in (("y0", 0), ("y1", 1), ("ylast", k - 1)):
+            assert abs(y[i] - c[key]) <= 1e-15 * abs(c[key]), (N, k, key, y[i], c[key])
+
+
+def test_small_x_rank25():
+    """SURVEY.md App. B regime: N = 25 with x ~ 1e-7 (x^24 ~ 1e-168 stays normal).
+    Homogeneity of degree N-1 (P10) ties it to the x ~ 1 case exactly up to rounding, and
+    k = 2 / k = N closed forms (P5, P6) pin single edges at that scale."""
+    rng = np.random.default_rng(25)
+    edges = [sorted(rng.choice(40, size=int(k), replace=False).tolist()) for k in (2, 3, 5, 8, 12, 25, 4, 6)]
+    x = rng.uniform(0.2, 1.0, 40)
+    hg = to_hg(40, 25, edges, rng.uniform(0.5, 1.5, len(edges)), x)
+    a = 1e-7
+    y1 = oracle.sttsv(hg)
+    ya = oracle.sttsv(hg, x=a * x)
+    assert np.all(np.abs(ya[y1 > 0]) > 0)
+    assert rel_err(ya / a ** 24, y1) < 1e-14
+    xs = a * x
+    y = oracle.sttsv(to_hg(40, 25, [[3, 7]], [1.0], xs))
+    for v, u in ((3, 7), (7, 3)):
+        ref = float((Fraction(xs[u]) + Fraction(xs[v])) ** 24 - Fraction(xs[v]) ** 24) / (2 ** 25 - 2)
+        assert abs(y[v] - ref) <= 1e-14 * abs(ref)
+    e = list(range(25))
+    y = oracle.sttsv(to_hg(40, 25, [e], [2.0], xs))
+    for v in (0, 11, 24):
+        ref = 2.0 / 25 * float(np.prod([Fraction(xs[u]) for u in e if u != v]))
+        assert abs(y[v] - ref) <= 1e-14 * abs(ref)
+
+
+def test_nqz_lambda_bracket_independent():
+    """The lambda bracket (Alg. 1 lines 8-9) against a direct exact-rational evaluation of
+    min/max z_v / x_v^(N-1) over x_v > 0 on a small graph with an isolated vertex."""
+    rng = np.random.default_rng(9)
+    n, N = 9, 5
+    edges = [sorted(rng.choice(8, size=int(rng.integers(2, N + 1)), replace=False).tolist()) for _ in range(14)]
+    hg = to_hg(n, N, edges, rng.uniform(0.5, 2.0, len(edges)), np.zeros(n))      # vertex 8 isolated
+    x, z, lo, hi, it = oracle.nqz(hg, tau=0.0, max_iters=3)
+    assert x[8] == 0 and z[8] == 0
+    ratios = [Fraction(z[v]) / Fraction(x[v]) ** (N - 1) for v in range(n) if x[v] > 0]
+    assert abs(lo - float(min(ratios))) <= 1e-15 * abs(lo) and abs(hi - float(max(ratios))) <= 1e-15 * abs(hi)
+
+
+def test_sttsv_vertices_against_brute_force():
+    """oracle.sttsv_vertices (the per-vertex form the full-size tests sample) against the
+    exact-rational brute force on random small instances, every vertex, and against the full
+    apply on a config-shaped input (hot and cold vertices)."""
+    rng = np.random.default_rng(77)
+    for it in range(25):
+        n, N, edges, w, x = random_instance(rng, integer=(it % 2 == 0))
+        exact = [float(v) for v in brute_force(n, N, edges, w, x)]
+        hg = to_hg(n, N, edges, w, x)
+        assert rel_err(oracle.sttsv_vertices(hg, np.arange(n)), exact) < 1e-14, it
+    hg = W.generate("centrality", m=3000, n=30_000)
+    deg = np.bincount(hg.indices, minlength=hg.n)
+    verts = np.concatenate([np.argsort(-deg)[:40], np.where(deg == 1)[0][:20], np.where(deg == 0)[0][:5]])
+    y = oracle.sttsv(hg)
+    got = oracle.sttsv_vertices(hg, verts)
+    assert np.all(np.abs(got - y[verts]) <= 1e-15 * np.abs(y[verts]))
