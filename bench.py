@@ -148,8 +148,28 @@ def oracle_sample(hg, target_s, calib_edges=200_000, attempts=4):
     return sub.incidences / dt, dt, desc, oracle.num_threads(), sub
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def workload_config(args, hg, world):
+    """The `config` dict both arms print (same keys and values: the workload only)."""
+    return {"workload": args.config, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank, "incidences": hg.incidences,
+            "l2": "inputs larger than L2 (126 MB): the hyperedge stream is read from HBM every step"
+                  if args.config in ("large", "centrality", "high-rank") else
+                  "inputs smaller than L2: the stream may stay L2-resident between steps",
+            "parallelism": "edge-sharded x%d%s" % (world, " + NCCL allreduce of y_active" if world > 1 else "")}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     import oracle
@@ -168,9 +188,9 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": args.config, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank,
-                      "sample_incidences_per_step": sub.incidences},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+           "config": workload_config(args, hg, world),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(),
+                            "kind": "oracle", "sample": desc, "sample_incidences_per_step": sub.incidences},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -188,23 +208,32 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # --no-comm: the multi-rank harness (sharding, barriers, max-over-ranks timing) without
+    # the NCCL data plane: each rank's plan returns its shard's partial sum and rank 0
+    # checks the host-side sum of the partials.  Ranks may share one GPU (device =
+    # LOCAL_RANK mod device count): their kernels never wait on each other.
+    ndev = torch.cuda.device_count()
+    dev_index = local % ndev if args.no_comm else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.no_comm:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.perf_counter()
     hg = W.generate(args.config)
     log(f"[rank {rank}] generated {args.config}: m={hg.m} incidences={hg.incidences} in {time.perf_counter()-t0:.1f}s")
     comm = None
-    if world > 1:
+    if world > 1 and not args.no_comm:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(S.sttsv_comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, src=0)
-        comm = S.sttsv_comm_create(bytes(uid.cpu().tolist()), world, rank, local)
+        comm = S.sttsv_comm_create(bytes(uid.cpu().tolist()), world, rank, dev_index)
     t0 = time.perf_counter()
-    plan = S.Plan.from_hypergraph(hg, device=local, world=world, rank=rank, comm=comm)
+    plan = S.Plan.from_hypergraph(hg, device=dev_index, world=world, rank=rank, comm=comm)
     info = plan.info()
     log(f"[rank {rank}] plan in {time.perf_counter()-t0:.1f}s: {json.dumps({k: v for k, v in info.items() if k != 'edges_per_size'})}")
 
@@ -213,34 +242,64 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
+        if world > 1:
+            if args.no_comm:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[dev_index])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if args.no_comm else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
     for _ in range(args.warmup):
         plan.apply(x, y, stream)
     barrier()
-    sampler = ClockSampler(local)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ---------------- headline: K applies, no library profiling inside the timed region;
+    # one event per step boundary (events add no GPU work) for min / median per step
+    sampler = ClockSampler(dev_index)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with sampler:
-        plan.profile(True)
         barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             plan.apply(x, y, stream)
-        ev1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        plan.profile(False)
-    ms_total = ev0.elapsed_time(ev1)
-    kern_ms, kern_n = plan.profile_read()
-    kern_avg = kern_ms / max(kern_n, 1)
-    if world > 1:
-        t = torch.tensor([ms_total, kern_avg], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, kern_avg = t.tolist()
+    ms_total = evs[0].elapsed_time(evs[-1])
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms_total, ms_min, ms_med = max_over_ranks([ms_total, min(per_step), statistics.median(per_step)])
     ms_step = ms_total / args.steps
     value = hg.incidences / (ms_step * 1e-3)
+
+    # ---------------- separate profiled pass: edge-kernel time from library events
+    plan.profile(True)
+    for _ in range(args.steps):
+        plan.apply(x, y, stream)
+    torch.cuda.synchronize(dev)
+    plan.profile(False)
+    kern_ms, kern_n = plan.profile_read()
+    kern_avg = max_over_ranks([kern_ms / max(kern_n, 1)])[0]
+
+    shard_check = None
+    if world > 1 and args.no_comm:
+        # host-side sum of the shards' partial products against a one-shard plan
+        plan.apply(x, y, stream)
+        part = y.cpu()
+        dist.all_reduce(part)
+        if rank == 0:
+            full = S.Plan.from_hypergraph(hg, device=dev_index)
+            yf = full.apply(x).cpu()
+            full.close()
+            err = float((part - yf).abs().max() / yf.abs().max())
+            shard_check = {"rel_linf_vs_one_shard": err, "ok": err <= 1e-12,
+                           "what": "sum over ranks of the comm-less shard plans' y vs a world=1 plan"}
 
     # ---------------- end to end through the public host-buffer call (sttsv_apply_host)
     xh = torch.from_numpy(hg.x.copy()).pin_memory()
@@ -253,11 +312,7 @@ def run_ours(args):
     for _ in range(e2e_steps):
         plan.apply_host(xh_np, yh_np)
     barrier()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = t.item()
+    e2e_s = max_over_ranks([(time.perf_counter() - t0) / e2e_steps])[0]
     sparse_x = info["n_active"] * 8 <= hg.n   # sttsv_apply_host copies only x on the active vertices
     e2e = {"value": hg.incidences / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(info["n_active"] * 8 if sparse_x else xh.numel() * 8),
@@ -268,120 +323,107 @@ def run_ours(args):
                      "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
 
     # ---------------- roofline of the dominant kernel (edge kernel)
-    # algorithmic bytes per SURVEY.md 8(d): the int32-id / fp64-weight store; the
-    # plan may stream the ids as uint16 (n_active <= 65536), reported separately
+    # binding roof = the larger of (bytes the kernel actually streams / HBM peak) and
+    # (FP64 flops / FP64 peak); the SURVEY.md 8(d) int32-id byte count is secondary
     alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
     phys_bytes = info["id_bytes"] * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
     peak, peak_src = measured_peaks()
-    achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
     fp64_peak, fp64_src = fp64_peak_tflops()
-    fp64_tf = 2.0 * info["fma_per_apply"] / (kern_avg * 1e-3) / 1e12
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config), "kernel": "sttsv::edge_kernel<N>",
-                "kernel_ms": kern_avg, "kernel_share_of_step": kern_avg / ms_step,
-                "alg_bytes_per_launch": alg_bytes,
-                "alg_bytes_def": "SURVEY.md 8(d), int32/fp64 store: 4*sum|e| (ids) + 8*m (fp64 w') + 8*n_active (x_a) "
-                                 "+ 8*n_active (y_a) per shard",
-                "stream": {"id_bytes": info["id_bytes"], "bytes_per_launch": phys_bytes,
-                           "gbs": phys_bytes / (kern_avg * 1e-3) / 1e9,
-                           "frac": phys_bytes / (kern_avg * 1e-3) / 1e9 / peak,
-                           "note": "bytes the kernel actually streams: member ids as uint16 when n_active <= 65536 "
-                                   "(every relabelled id fits); compare with traffic"},
-                "peak_source": peak_src,
-                "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_tf / fp64_peak,
-                         "peak_source": fp64_src,
-                         "flops_def": "2 x (FMAs of the per-edge DP, SURVEY.md App. A, + k+1 scalings) per edge; "
-                                      "the series table is per active vertex per apply"}}
+    ksec = kern_avg * 1e-3
+    stream_gbs = phys_bytes / ksec / 1e9
+    fp64_tf = 2.0 * info["fma_per_apply"] / ksec / 1e12
+    stream_frac, fp64_frac = stream_gbs / peak, fp64_tf / fp64_peak
+    traffic = ncu_traffic(args.config)
+    if stream_frac >= fp64_frac:
+        head = {"bound": "hbm", "achieved": stream_gbs, "peak": peak, "unit": "GB/s", "frac": stream_frac}
+    else:
+        head = {"bound": "alu", "achieved": fp64_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": fp64_frac}
+    roofline = dict(head)
+    roofline.update({
+        "traffic": traffic, "kernel": "sttsv::edge_kernel<N>", "kernel_ms": kern_avg,
+        "kernel_share_of_step": kern_avg / ms_step,
+        "binding": {"frac": max(stream_frac, fp64_frac), "hbm_stream_frac": stream_frac, "fp64_frac": fp64_frac,
+                    "note": "primary figure: the larger of the two roofs the kernel is held to; 'alu' = the "
+                            "FP64 DFMA pipe"},
+        "stream": {"id_bytes": info["id_bytes"], "bytes_per_launch": phys_bytes, "gbs": stream_gbs,
+                   "frac": stream_frac, "peak_source": peak_src,
+                   "note": "bytes the kernel streams (member ids as uint16 when n_active <= 65536) + x_a/y_a; "
+                           "compare with traffic (ncu DRAM bytes per launch)"},
+        "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_frac, "peak_source": fp64_src,
+                 "flops_def": "2 x (FMAs of the per-edge DP, SURVEY.md App. A, + k+1 scalings) per edge"},
+        "hbm_alg": {"bytes_per_launch": alg_bytes, "gbs": alg_bytes / ksec / 1e9, "frac": alg_bytes / ksec / 1e9 / peak,
+                    "def": "secondary: SURVEY.md 8(d) algorithmic bytes of the int32/fp64 store: 4*sum|e| + 8*m "
+                           "+ 16*n_active per shard"}})
 
     # ---------------- secondary: the same product with STTSV_MERGE_DUPLICATES
     # (identical vertex sets merged at plan time, weights summed; B is linear in
     # w).  Reported beside the headline, never as it: the headline stores and
     # processes every input hyperedge.
-    merged = None
-    if not args.no_merge_report:
-        mplan = S.Plan.from_hypergraph(hg, device=local, world=world, rank=rank, comm=comm,
-                                       flags=S.STTSV_MERGE_DUPLICATES)
-        minfo = mplan.info()
+    def time_loop(fn):
         for _ in range(args.warmup):
-            mplan.apply(x, y, stream)
+            fn()
         barrier()
-        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        m0.record(stream)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
         for _ in range(args.steps):
-            mplan.apply(x, y, stream)
-        m1.record(stream)
+            fn()
+        b1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        mms = m0.elapsed_time(m1) / args.steps
-        if world > 1:
-            t = torch.tensor([mms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            mms = t.item()
+        return max_over_ranks([b0.elapsed_time(b1) / args.steps])[0]
+
+    merged = None
+    if not args.no_merge_report:
+        mplan = S.Plan.from_hypergraph(hg, device=dev_index, world=world, rank=rank, comm=comm,
+                                       flags=S.STTSV_MERGE_DUPLICATES)
+        minfo = mplan.info()
+        mms = time_loop(lambda: mplan.apply(x, y, stream))
         merged = {"value": hg.incidences / (mms * 1e-3), "unit": UNIT, "ms_per_step": mms,
                   "stored_edges": minfo["stored_edges"] * world, "input_edges": hg.m,
                   "note": "STTSV_MERGE_DUPLICATES plan (input incidences / time); not the headline"}
         mplan.close()
 
-    # ---------------- secondary: f4 batched apply of 4 vectors, both strategies:
-    # the default (one single-vector pass per vector) and STTSV_BATCH_FUSED (one
-    # pass over the edge stream for all vectors)
+    # ---------------- secondary: f4 batched apply of 4 vectors, both strategies
     batch = None
     if not args.no_batch_report:
         nv = 4
         X = x.unsqueeze(0).repeat(nv, 1)
         Y = torch.empty_like(X)
-
-        def time_batch(pl):
-            for _ in range(args.warmup):
-                pl.apply_batch(X, Y, stream)
-            barrier()
-            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            b0.record(stream)
-            for _ in range(args.steps):
-                pl.apply_batch(X, Y, stream)
-            b1.record(stream)
-            torch.cuda.synchronize(dev)
-            barrier()
-            ms = b0.elapsed_time(b1) / args.steps
-            if world > 1:
-                t = torch.tensor([ms], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = t.item()
-            return ms
-
-        bms = time_batch(plan)
-        fplan = S.Plan.from_hypergraph(hg, device=local, world=world, rank=rank, comm=comm,
+        bms = time_loop(lambda: plan.apply_batch(X, Y, stream))
+        fplan = S.Plan.from_hypergraph(hg, device=dev_index, world=world, rank=rank, comm=comm,
                                        flags=S.STTSV_BATCH_FUSED)
-        fms = time_batch(fplan)
+        fms = time_loop(lambda: fplan.apply_batch(X, Y, stream))
         fplan.close()
         del fplan
         batch = {"vectors": nv, "value": nv * hg.incidences / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms,
+                 "single_apply_ms": ms_step,
                  "fused": {"value": nv * hg.incidences / (fms * 1e-3), "ms_per_step": fms},
                  "note": "sttsv_apply_batch (SURVEY.md f4): vector-incidences/s; default = one pass per vector, "
                          "fused = STTSV_BATCH_FUSED (one pass over the edge stream); not the headline"}
         del X, Y
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         rate, dt, desc, threads, _ = oracle_sample(hg, args.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
-               "seconds": dt}
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": "oracle",
+               "sample": desc, "seconds": dt}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+               "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_min": ms_min,
+               "ms_per_step_median": ms_med, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": args.config, "n": hg.n, "m": hg.m, "rank_Nk": hg.rank,
-                          "incidences": hg.incidences, "n_active": info["n_active"],
-                          "l2": "inputs larger than L2: the %.2f GB edge stream is read once per step"
-                                % (info["stream_bytes"] * world / 1e9),
-                          "parallelism": "edge-sharded x%d%s" % (world, " + NCCL allreduce of y_active"
-                                                                 if world > 1 else ""),
-                          "kernel_grid": info["kernel_grid"], "kernel_block": info["kernel_block"],
-                          "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
-                          / (ms_step * 1e-3) / 1e9},
+               "config": workload_config(args, hg, world),
+               "launch": {"kernel_grid": info["kernel_grid"], "kernel_block": info["kernel_block"],
+                          "n_active": info["n_active"], "stream_bytes_per_shard": info["stream_bytes"],
+                          "comm": "nccl" if comm is not None else ("none (--no-comm: host-side shard sum)"
+                                                                    if world > 1 else "none")},
+               "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
+               / (ms_step * 1e-3) / 1e9,
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "merge_duplicates": merged, "batch": batch,
                "gpu_launches": plan.launches() * args.steps, "clocks": sampler.summary()}
+        if shard_check is not None:
+            out["shard_check"] = shard_check
         print(json.dumps(out), flush=True)
     plan.close()
     if comm is not None:
@@ -402,6 +444,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merge-report", action="store_true")
     ap.add_argument("--no-batch-report", action="store_true")
+    ap.add_argument("--no-comm", action="store_true",
+                    help="N>1 harness without the NCCL data plane (ranks may share a GPU; host-side shard sum)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 and "OMP_NUM_THREADS" not in os.environ:

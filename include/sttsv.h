@@ -102,9 +102,11 @@ enum {
  *            cardinality bucket k, in input order.  Every rank must pass the
  *            same full edge list.
  *  comm      NULL, or a communicator from sttsv_comm_create with the same
- *            world/rank: sttsv_apply then all-reduces the active part of y
- *            over NCCL so every rank returns the full s.  With world > 1 and
- *            comm == NULL, sttsv_apply returns only this shard's partial sum.
+ *            world/rank: every sttsv_apply (and every power / HEC step) then
+ *            all-reduces the active part of y over NCCL (one ncclAllReduce,
+ *            also at world = 1) so every rank returns the full s.  With
+ *            world > 1 and comm == NULL, sttsv_apply returns only this
+ *            shard's partial sum.
  *  flags     STTSV_CANONICALIZE, STTSV_MERGE_DUPLICATES, STTSV_DETERMINISTIC.
  *
  * The host arrays are copied; the caller may free them on return.  The plan
@@ -116,8 +118,10 @@ sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_t rank_Nk, 
                                  const int32_t* sizes, const int32_t* indices, const double* weights,
                                  int device, int world, int rank, sttsv_comm_t comm, uint32_t flags);
 
-/* Release the plan and its device memory (waits for its pending work).
- * NULL is accepted and ignored. */
+/* sttsv_destroy — release the plan and its device memory (waits for its
+ * pending work).  NULL is accepted and ignored.  (north_star's name;
+ * sttsv_plan_destroy is the same call under its round-1 name.) */
+sttsv_status_t sttsv_destroy(sttsv_plan_t plan);
 sttsv_status_t sttsv_plan_destroy(sttsv_plan_t plan);
 
 /* sttsv_apply — y = B x^{N-1} (Eq. (2)).
@@ -203,6 +207,7 @@ typedef struct {
   int32_t kernel_block;    /* threads per CTA of the edge kernel                         */
   int32_t id_bytes;        /* bytes per member id in the edge stream: 2 when n_active <= 65536
                               on ranks <= 12, else 4                                      */
+  int64_t allreduces;      /* ncclAllReduce calls this plan has issued (0 without a comm) */
 } sttsv_plan_info_t;
 
 sttsv_status_t sttsv_plan_info(sttsv_plan_t plan, sttsv_plan_info_t* info);

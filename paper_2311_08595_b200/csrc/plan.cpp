@@ -249,6 +249,7 @@ struct sttsv_plan_s {
   size_t smem = 0;
   int64_t stream_bytes = 0;
   double fma = 0;
+  int64_t allreduces = 0;  // ncclAllReduce calls issued (sttsv_plan_info)
   // edge-kernel timing (sttsv_plan_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
@@ -322,10 +323,12 @@ static void free_plan(sttsv_plan_s* p) {
   delete p;
 }
 
-extern "C" sttsv_status_t sttsv_plan_destroy(sttsv_plan_t p) {
+extern "C" sttsv_status_t sttsv_destroy(sttsv_plan_t p) {
   free_plan(p);
   return STTSV_OK;
 }
+
+extern "C" sttsv_status_t sttsv_plan_destroy(sttsv_plan_t p) { return sttsv_destroy(p); }
 
 extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_t N, int64_t m,
                                             const int32_t* sizes, const int32_t* indices, const double* weights,
@@ -752,6 +755,7 @@ extern "C" sttsv_status_t sttsv_plan_info(sttsv_plan_t p, sttsv_plan_info_t* inf
   info->kernel_grid = p->grid;
   info->kernel_block = p->block;
   info->id_bytes = p->ent.id_bytes;
+  info->allreduces = p->allreduces;
   return STTSV_OK;
 }
 
@@ -823,10 +827,13 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
   if (p->det)  // fixed-order sums of the vertex-major buffer (every active vertex written)
     CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk, p->d_ya,
                                p->n_active, s), "deterministic reduce launch");
-  if (p->comm && p->world > 1) {
+  // a6: the one exchange step, whenever a communicator is
+  // attached (also at world = 1, where NCCL reduces over a single rank)
+  if (p->comm) {
     NcclApi* api = nccl_api();
     ncclResult_t r = api->AllReduce(p->d_ya, p->d_ya, (size_t)p->n_active, ncclFloat64, ncclSum, p->comm->comm, s);
     if (r != ncclSuccess) return fail(STTSV_ERR_NCCL, "ncclAllReduce: %s", api->GetErrorString(r));
+    ++p->allreduces;
   }
   return STTSV_OK;
 }
@@ -1060,10 +1067,11 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,
                                              p->b_ya, na, s), "deterministic reduce launch");
     }
-    if (p->comm && p->world > 1) {
+    if (p->comm) {
       NcclApi* api = nccl_api();
       ncclResult_t r = api->AllReduce(p->b_ya, p->b_ya, (size_t)nvec * na, ncclFloat64, ncclSum, p->comm->comm, s);
       if (r != ncclSuccess) return fail(STTSV_ERR_NCCL, "ncclAllReduce: %s", api->GetErrorString(r));
+      ++p->allreduces;
     }
   }
   for (int v = 0; v < nvec; ++v) {

@@ -44,7 +44,7 @@ class PlanInfo(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("stream_bytes", ctypes.c_int64),
                 ("fma_per_apply", ctypes.c_double), ("hot_private", ctypes.c_int32),
                 ("hot_shared", ctypes.c_int32), ("kernel_grid", ctypes.c_int32), ("kernel_block", ctypes.c_int32),
-                ("id_bytes", ctypes.c_int32)]
+                ("id_bytes", ctypes.c_int32), ("allreduces", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "edges_per_size"}
@@ -69,6 +69,7 @@ def load():
     sig = {
         "sttsv_plan_create": ([ctypes.POINTER(P), i64, i32, i64, P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
                                u32], st),
+        "sttsv_destroy": ([P], st),
         "sttsv_plan_destroy": ([P], st),
         "sttsv_apply": ([P, P, P, P], st),
         "sttsv_apply_host": ([P, P, P], st),
@@ -97,7 +98,7 @@ def load():
 
 
 def exported_symbols() -> list[str]:
-    return ["sttsv_plan_create", "sttsv_plan_destroy", "sttsv_apply", "sttsv_apply_host", "sttsv_apply_batch",
+    return ["sttsv_plan_create", "sttsv_destroy", "sttsv_plan_destroy", "sttsv_apply", "sttsv_apply_host", "sttsv_apply_batch",
             "sttsv_power_iterate",
             "sttsv_hec",
             "sttsv_plan_info", "sttsv_apply_launches", "sttsv_plan_profile", "sttsv_plan_profile_read",
@@ -137,6 +138,10 @@ def sttsv_plan_create(n, rank_Nk, sizes, indices, weights=None, device=0, world=
     _check(lib.sttsv_plan_create(ctypes.byref(h), int(n), int(rank_Nk), len(sizes), _ptr(sizes), _ptr(indices),
                                  _ptr(w), int(device), int(world), int(rank), comm, int(flags)))
     return h
+
+
+def sttsv_destroy(plan):
+    _check(load().sttsv_destroy(plan))
 
 
 def sttsv_plan_destroy(plan):
@@ -288,6 +293,9 @@ class Plan:
             raise ValueError("x must have shape (n,)")
         if y is None:
             y = np.empty(self.n, dtype=np.float64)
+        elif not (isinstance(y, np.ndarray) and y.dtype == np.float64 and y.shape == (self.n,)
+                  and y.flags.c_contiguous and y.flags.writeable):
+            raise ValueError("y must be a writeable C-contiguous float64 ndarray of shape (n,)")
         sttsv_apply_host(self._h, x, y)
         return y
 
@@ -318,7 +326,7 @@ class Plan:
 
     def close(self):
         if getattr(self, "_h", None):
-            sttsv_plan_destroy(self._h)
+            sttsv_destroy(self._h)
             self._h = None
 
     def __del__(self):

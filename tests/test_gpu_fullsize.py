@@ -1,0 +1,131 @@
+"""GPU parity at BASELINE.json's FULL sizes, element by element on every vertex.
+
+north_star: "GPU STTSV matching the oracle within 1e-11 relative on all five
+configs".  Each config is generated at its full size and applied with the plan
+bench.py times (default flags, the same launch configuration); the whole output
+vector is compared with the oracle's (§II Eq. (2) on the
+blowup tensor):
+
+* rel L-inf  max_v |y_gpu - y_ora| / max_v |y_ora| <= 1e-11 (reading A16);
+* the 64 hottest vertices (the ones the register runs, per-CTA L2 slices and
+  the slice fold carry) each to 1e-12 relative;
+* exact zeros off the active set (a vertex in no hyperedge has no tensor entry,
+  PAPER.md:343).
+
+tiny, mid, large and one centrality apply run the oracle live (seconds on the
+GPU host's cores).  high-rank (1.2e12 kappa terms) and the 50-step centrality
+power iteration (Alg. 1 lines 3-6, reading A14) compare with
+results the oracle computed once (tools/make_oracle_cache.py, which calls only
+oracle/ and workloads/), stored under tests/golden/ with the sha256 of the
+generated input; a key mismatch fails the test.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+HOT_TOL = 1e-12
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2311_08595_b200 as S
+    return S
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def cached(name, hg):
+    path = os.path.join(GOLDEN, f"oracle_{name}.npz")
+    assert os.path.exists(path), f"missing {path}: run tools/make_oracle_cache.py {name}"
+    d = np.load(path)
+    assert str(d["key"]) == W.input_key(hg), f"{path} was computed for a different input"
+    return d
+
+
+def dense(n, support, vals):
+    out = np.zeros(n)
+    out[support] = vals
+    return out
+
+
+def check_vector(got, ref, deg, what):
+    assert rel(got, ref) <= TOL, (what, rel(got, ref))
+    hot = np.argsort(-deg, kind="stable")[:64]
+    err = np.abs(got[hot] - ref[hot]) / np.abs(ref[hot])
+    assert np.all(err <= HOT_TOL), (what, int(hot[np.argmax(err)]), float(err.max()))
+    iso = deg == 0
+    assert np.all(got[iso] == 0.0), what
+
+
+def gpu_apply(S, torch, hg):
+    plan = S.Plan.from_hypergraph(hg)
+    x = torch.from_numpy(hg.x).cuda()
+    y = plan.apply(x)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), plan
+
+
+@pytest.mark.parametrize("name", ["tiny", "mid", "large", "centrality", "high-rank"])
+def test_full_size_every_vertex(S, torch_cuda, name):
+    hg = W.generate(name)
+    deg = np.bincount(hg.indices, minlength=hg.n)
+    y, plan = gpu_apply(S, torch_cuda, hg)
+    info = plan.info()
+    assert info["total_incidences"] == hg.incidences and info["num_edges"] == hg.m
+    plan.close()
+    if name == "high-rank":
+        d = cached(name, hg)
+        ref = dense(hg.n, d["support"], d["y"])
+        assert np.array_equal(np.asarray(d["support"]), np.nonzero(deg)[0])
+    else:
+        ref = oracle.sttsv(hg)
+    check_vector(y, ref, deg, name)
+
+
+def test_centrality_power_iteration_full(S, torch_cuda):
+    """x_50 and z_50 of the centrality config (50 x-updates from x_0 = 1/n) at full size."""
+    torch = torch_cuda
+    hg = W.generate("centrality")
+    d = cached("centrality", hg)
+    deg = np.bincount(hg.indices, minlength=hg.n)
+    plan = S.Plan.from_hypergraph(hg)
+    x = torch.full((hg.n,), 1.0 / hg.n, dtype=torch.float64, device="cuda")
+    x, z = plan.power_iterate(x, 50)
+    torch.cuda.synchronize()
+    xg, zg = x.cpu().numpy(), z.cpu().numpy()
+    plan.close()
+    check_vector(xg, dense(hg.n, d["support"], d["x"]), deg, "x50")
+    check_vector(zg, dense(hg.n, d["support"], d["z"]), deg, "z50")
+    assert abs(xg.sum() - 1.0) < 1e-12
+
+
+def test_high_rank_small_x(S, torch_cuda):
+    """SURVEY.md App. B regime at N = 25: x ~ 1e-7 (x^24 ~ 1e-168), on the high-rank
+    structure (reduced m so the oracle runs live)."""
+    torch = torch_cuda
+    hg = W.generate("high-rank", m=3000)
+    xs = 1e-7 * hg.x
+    plan = S.Plan.from_hypergraph(hg)
+    y = plan.apply(torch.from_numpy(xs).cuda()).cpu().numpy()
+    ref = oracle.sttsv(hg, x=xs)
+    deg = np.bincount(hg.indices, minlength=hg.n)
+    assert np.max(np.abs(ref)) > 0
+    check_vector(y, ref, deg, "high-rank x*1e-7")
+    plan.close()

@@ -23,7 +23,6 @@ interrupted run resumes.
 from __future__ import annotations
 
 import argparse
-import hashlib
 import json
 import os
 import sys
@@ -41,13 +40,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 CKPT = os.path.join(ROOT, "gpurun_out", "oracle_ckpt")
 
 
-def input_key(hg) -> str:
-    h = hashlib.sha256()
-    h.update(np.array([hg.n, hg.rank], dtype=np.int64).tobytes())
-    for a in (hg.sizes.astype(np.int32), hg.indices.astype(np.int32), hg.weights.astype(np.float64),
-              hg.x.astype(np.float64)):
-        h.update(np.ascontiguousarray(a).tobytes())
-    return h.hexdigest()
+input_key = W.input_key
 
 
 def high_rank(chunks: int):

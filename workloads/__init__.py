@@ -234,6 +234,18 @@ def random_small(rng: np.random.Generator, n: int, m: int, rank: int, kmin: int 
     return Hypergraph(n, rank, sizes, _offsets(sizes), idx, w, x, "random")
 
 
+def input_key(hg: Hypergraph) -> str:
+    """sha256 of a generated input (n, N, sizes, indices, weights, x): the key under which
+    stored oracle results (tests/golden/oracle_*.npz) are filed."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.array([hg.n, hg.rank], dtype=np.int64).tobytes())
+    for a in (hg.sizes.astype(np.int32), hg.indices.astype(np.int32), hg.weights.astype(np.float64),
+              hg.x.astype(np.float64)):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
 def uniform_draws(seed: int, stream: int, count: int) -> np.ndarray:
     out = np.empty(count, dtype=np.float64)
     _load().gen_uniform(seed, stream, count, _ptr(out))
