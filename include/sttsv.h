@@ -76,9 +76,12 @@ enum {
                                        plan-time slot of a vertex-major buffer and summed in a fixed order
                                        (no atomics); costs ~12 B more per incidence per apply, needs
                                        < 2^31 incidences per shard; not with STTSV_BATCH_FUSED nvec > 1 */
-  STTSV_BATCH_FUSED = 1u << 3       /* sttsv_apply_batch runs ONE pass over the hyperedge stream for all
+  STTSV_BATCH_FUSED = 1u << 3,      /* sttsv_apply_batch runs ONE pass over the hyperedge stream for all
                                        vectors (the fused batch kernel) instead of one sttsv_apply pass
                                        per vector; see sttsv_apply_batch for when each is faster       */
+  STTSV_NO_PREFIX_MEMO = 1u << 4    /* turn off the shared-prefix memo: every
+                                       edge runs its full per-edge DP and streams all its ids (for A/B
+                                       measurements; the memo is on by default)                        */
 };
 
 /* ------------------------------------------------------------------ plans */
@@ -208,6 +211,12 @@ typedef struct {
   int32_t id_bytes;        /* bytes per member id in the edge stream: 2 when n_active <= 65536
                               on ranks <= 12, else 4                                      */
   int64_t allreduces;      /* ncclAllReduce calls this plan has issued (0 without a comm) */
+  double  fma_executed;    /* FP64 operations the edge kernel executes per apply: fma_per_apply minus
+                              what the shared-prefix memo saves                 */
+  int64_t prefix_tiles;    /* tiles whose edges share a member prefix (its id columns are not streamed) */
+  int64_t prefix_groups;   /* runs of consecutive such tiles with the same prefix                  */
+  int64_t prefix_incidences; /* incidences that lie in a shared prefix                            */
+  int64_t num_tiles;       /* tiles of the edge stream                                            */
 } sttsv_plan_info_t;
 
 sttsv_status_t sttsv_plan_info(sttsv_plan_t plan, sttsv_plan_info_t* info);

@@ -45,6 +45,7 @@
 
 #include "dp.cuh"
 #include "internal.h"
+#include "prefix.cuh"
 
 namespace sttsv {
 
@@ -63,7 +64,8 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 
 // ---- compile-time tuning (each default was chosen by A/B timing on B200 with
 // tools/variants.py + tools/time_apply.py)
-// small ranks (N <= 10): two CTAs per SM, each 8 (N <= 8) or 7 consumer warps + 1 producer
+// small ranks (N <= 10): two CTAs per SM, each 7 consumer warps + 1 producer (8 spill
+// under the two-CTA register cap once the shared-prefix paths are compiled in)
 // with a 112 KB ring (two independent TMA pipelines per SM measured 2.7% faster
 // than one CTA of 15 consumers on `large`), 5 edges per lane per tile
 #ifndef STTSV_EPL
@@ -77,7 +79,7 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #define STTSV_RING_KB 112
 #endif
 #ifndef STTSV_NCW_SMALL
-#define STTSV_NCW_SMALL 8
+#define STTSV_NCW_SMALL 7
 #endif
 // N = 9, 10: 7 consumer warps (8 would spill under the two-CTA register cap)
 #ifndef STTSV_NCW_SMALL9
@@ -115,6 +117,11 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #ifndef STTSV_BIG_NORM
 #define STTSV_BIG_NORM 1
 #endif
+// shared-prefix memo (prefix.cuh): a tile whose edges share a prefix of U members
+// runs the DP over its M = K - U own members, M <= PREFIX_MMAX
+#ifndef STTSV_PREFIX_MMAX
+#define STTSV_PREFIX_MMAX 4
+#endif
 // suspend-time hint (ns) of the producer's mbarrier waits
 #ifndef STTSV_WAIT_HINT_NS
 #define STTSV_WAIT_HINT_NS 1000000
@@ -150,6 +157,9 @@ struct EdgeCfg {
   static constexpr int SLOTS = 8;
   static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = BIG ? 1 : (N <= 10 ? STTSV_MIN_BLOCKS : STTSV_MID_BLOCKS);
+  // shared-prefix memo limits (0: off on this path)
+  static constexpr int PMAX = (BIG || N < STTSV_NORM_MIN || !STTSV_MID_NORM) ? 0 : STTSV_PREFIX_MMAX;
+  static constexpr int PLMAX = BIG ? 0 : KMAX;  // (no limit on L on the unrolled path)
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
   static_assert(RING_BYTES >= 2 * STAGE_BYTES, "ring must hold two of the largest stages");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
@@ -341,6 +351,123 @@ __device__ __forceinline__ void dispatch_k(int k, const IdT* sids, const double*
       return;
     }
     dispatch_k<N, K + 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xg, ra, sk, ds, lane);
+  }
+}
+
+// Deposit of own members: slot OFF + i gets (id[i], dv[i]) (run accumulators as slots_deposit)
+template <int M, int OFF, int RMAX>
+__device__ __forceinline__ void slots_deposit_off(const int (&id)[M], const double (&dv)[M], RunAcc<RMAX>& ra,
+                                                  const Sink& sk) {
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    constexpr int R1 = RMAX - 1;
+    const int slot = OFF + i;
+    if (slot < RMAX) {
+      const int j = slot < RMAX ? slot : R1;
+      if (id[i] != ra.rid[j]) {
+        if (ra.rid[j] >= 0) red_add(sk.at(ra.rid[j]), ra.run[j]);
+        ra.rid[j] = id[i];
+        ra.run[j] = 0.0;
+      }
+      ra.run[j] += dv[i];
+    } else {
+      red_add(sk.at(id[i]), dv[i]);
+    }
+  }
+}
+
+// The warp's block of a staged tile whose edges share their first U = K - M
+// members (the stage holds only the M own id columns).  G: the tile's prefix
+// group in the per-apply group table (prefix.cuh: front A, the contraction
+// rows C_i and the prefix ids).  Each lane accumulates SB = sum_e w'_e B_e over
+// its edges; at the end of the block the warp sums SB and lane i < U deposits
+// member i's total  sum_j C_i[j] SB[j].
+template <int N, int K, int M, int TILE, int EPL, int RMAX, typename IdT>
+__device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, const double* __restrict__ sw,
+                                                  int base, const double* __restrict__ xg,
+                                                  const double* __restrict__ G, RunAcc<RMAX>& ra, const Sink& sk,
+                                                  int lane) {
+  constexpr int L = N - K + 1;
+  constexpr int GS = series_stride(N);
+  constexpr int U = K - M;
+  double sb[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) sb[j] = 0.0;
+  if constexpr (M == 0) {
+    // every edge of the tile is the same vertex set: SB = (sum w', 0, ...)
+#pragma unroll
+    for (int r = 0; r < EPL; ++r) sb[0] += sw[base + r * 32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sb[0] += __shfl_xor_sync(kFull, sb[0], o);
+  } else {
+    double a[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) a[j] = __ldg(G + j);  // front A (row format), the same on every lane
+#pragma unroll 1
+    for (int r = 0; r < EPL; ++r) {
+      const int col = base + r * 32 + lane;
+      int id[M];
+      double h[M][L];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        id[i] = (int)sids[i * TILE + col];
+        load_series<L>(xg + (size_t)(uint32_t)id[i] * GS, h[i]);
+      }
+      const double w = sw[col];
+      double q[M], F, bh[L];
+      dp_front_norm<M, L>(a, h, q, F, bh);
+      const double wF = w * F;
+      double dv[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) dv[i] = fma(w, q[i], wF);
+      slots_deposit_off<M, U, RMAX>(id, dv, ra, sk);
+      const double c = w * bh[0];
+      sb[0] += c;
+#pragma unroll
+      for (int j = 1; j < L; ++j) sb[j] = fma(c, bh[j], sb[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sb[j] += __shfl_xor_sync(kFull, sb[j], o);
+  }
+  if (lane < U) {
+    const double* C = G + L + lane * L;
+    double c = 0.0;
+    if constexpr (M == 0) {
+      c = __ldg(C) * sb[0];
+    } else {
+#pragma unroll
+      for (int j = 0; j < L; ++j) c = fma(__ldg(C + j), sb[j], c);
+    }
+    const long long v = __ldg(reinterpret_cast<const long long*>(G + L + U * L) + lane);
+    red_add(sk.at((int)v), c);
+  }
+}
+
+// prefix tiles of bucket K: dispatch on the number of own members M = K - U
+template <int N, int K, int M, int MMAX, int TILE, int EPL, int RMAX, typename IdT>
+__device__ __forceinline__ void dispatch_m(int m, const IdT* sids, const double* sw, int base, const double* xg,
+                                           const double* G, RunAcc<RMAX>& ra, const Sink& sk, int lane) {
+  if constexpr (M < K && M <= MMAX) {
+    if (m == M) {
+      warp_block_prefix<N, K, M, TILE, EPL, RMAX, IdT>(sids, sw, base, xg, G, ra, sk, lane);
+      return;
+    }
+    dispatch_m<N, K, M + 1, MMAX, TILE, EPL, RMAX, IdT>(m, sids, sw, base, xg, G, ra, sk, lane);
+  }
+}
+
+template <int N, int K, int MMAX, int TILE, int EPL, int RMAX, typename IdT>
+__device__ __forceinline__ void dispatch_kp(int k, int U, const IdT* sids, const double* sw, int base,
+                                            const double* xg, const double* G, RunAcc<RMAX>& ra, const Sink& sk,
+                                            int lane) {
+  if constexpr (K <= N) {
+    if (k == K) {
+      dispatch_m<N, K, 0, MMAX, TILE, EPL, RMAX, IdT>(K - U, sids, sw, base, xg, G, ra, sk, lane);
+      return;
+    }
+    dispatch_kp<N, K + 1, MMAX, TILE, EPL, RMAX, IdT>(k, U, sids, sw, base, xg, G, ra, sk, lane);
   }
 }
 
@@ -620,6 +747,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
   __shared__ uint32_t soff[SLOTS];  // byte offset of each slot's stage in the ring
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int64_t stile[SLOTS];  // tile index staged in each slot (-1: no more work)
+  __shared__ int64_t sgoff[SLOTS];  // its prefix group's offset in the group table ...
+  __shared__ uint8_t su[SLOTS];     // ... and shared-prefix length U (its first U id columns are not staged)
 
   for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) priv_cta[j] = 0.0;
   if (tid == 0) {
@@ -655,7 +784,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         if (t >= 0)
           while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const int k = t >= 0 ? p.b[b].k : 0;
-        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (Cfg::IDB * k + 8)) : 0u;
+        const int tu = (t >= 0 && p.tile_u) ? (int)__ldg(p.tile_u + t) : 0;
+        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (Cfg::IDB * (k - tu) + 8)) : 0u;
         uint64_t start = head;
         if (start % Cfg::RING_BYTES + need > (uint64_t)Cfg::RING_BYTES) start += Cfg::RING_BYTES - start % Cfg::RING_BYTES;
         while (it - oldest >= SLOTS || (oldest < it && start + need - tail > (uint64_t)Cfg::RING_BYTES)) {
@@ -669,6 +799,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         const uint32_t off = (uint32_t)(start % Cfg::RING_BYTES);
         soff[s] = off;
         stile[s] = t;
+        su[s] = (uint8_t)tu;
+        sgoff[s] = tu > 0 ? __ldg(p.goff + __ldg(p.tile_gid + t)) : 0;
         if (t < 0) {
           mbar_arrive_expect_tx(&full[s], 0);
           break;
@@ -679,9 +811,10 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         unsigned char* st = ring + off;
         const unsigned char* idp = reinterpret_cast<const unsigned char*>(p.ids);
         mbar_arrive_expect_tx(&full[s], need);
-        for (int i = 0; i < k; ++i)
-          bulk_g2s(st + i * id_bytes, idp + (size_t)(bd.ids_off + i * bd.stride + e0) * Cfg::IDB, id_bytes, &full[s]);
-        bulk_g2s(st + k * id_bytes, p.w + bd.w_off + e0, w_bytes, &full[s]);
+        for (int i = tu; i < k; ++i)  // the shared prefix columns 0..U-1 are not staged
+          bulk_g2s(st + (i - tu) * id_bytes, idp + (size_t)(bd.ids_off + i * bd.stride + e0) * Cfg::IDB, id_bytes,
+                   &full[s]);
+        bulk_g2s(st + (k - tu) * id_bytes, p.w + bd.w_off + e0, w_bytes, &full[s]);
       }
     }
   } else {
@@ -695,6 +828,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       ra.rid[i] = -1;  // empty run
       ra.run[i] = 0.0;
     }
+    constexpr bool PREFIX = Cfg::PMAX > 0 && !BATCH && !DET;
     int b = 0;
     bool any = false;
     // programmatic dependent launch: x_a, the series table and y_a are written
@@ -724,11 +858,23 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
 #endif
       const DetSink ds{DET ? p.slot + p.b[b].ids_off + (t - p.b[b].tile_begin) * TILE : nullptr, p.b[b].stride,
                        p.contrib};
+      const int tu = su[s];
       {
         const unsigned char* st = ring + soff[s];
         using IdT = typename std::conditional<Cfg::IDB == 2, uint16_t, int32_t>::type;
         const IdT* sids = reinterpret_cast<const IdT*>(st);
-        const double* sw = reinterpret_cast<const double*>(st + k * TILE * Cfg::IDB);
+        const double* sw = reinterpret_cast<const double*>(st + (k - tu) * TILE * Cfg::IDB);
+        if constexpr (PREFIX) {
+          // shared-prefix tiles (prefix.cuh): the DP over the own members, the
+          // prefix members' totals from the group table
+          if (tu > 0) {
+            dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT>(k, tu, sids, sw, warp * 32 * EPL, p.xg,
+                                                               p.gtab + sgoff[s], ra, sk, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            continue;
+          }
+        }
         // one pass per vector; with several vectors the runs of a pass are flushed
         // (warp-aggregated) at its end, with one they continue across tiles
         for (int v = 0; v < nvec; ++v) {

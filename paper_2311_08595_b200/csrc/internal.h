@@ -56,6 +56,13 @@ struct EdgeKernelParams {
   unsigned long long* tile_counter;
   int64_t chunk;         // tiles per grab
   int64_t guided_from;   // tile index after which grabs are single tiles
+  // shared-prefix memo (prefix.cuh; nullptr = off): per tile the number U of
+  // leading members all its edges share (their id columns are not streamed) and
+  // its prefix group (-1: U = 0)
+  const uint8_t* tile_u;
+  const int32_t* tile_gid;
+  const int64_t* goff;   // group -> offset of its record in gtab
+  const double* gtab;    // per-apply group table (prefix.cuh)
 };
 
 // Ranks with a fully unrolled edge kernel (one object file each); every other
@@ -77,6 +84,8 @@ struct EdgeKernelEntry {
   int table_norm;      // series table rows normalised to a leading 1 (dp.cuh series_row norm = 1)
   int epl;             // consecutive edges per lane per tile (lane l: columns l*epl .. l*epl+epl-1 of its warp block)
   int id_bytes;        // bytes per member id in the edge stream (4, or 2: plans with n_a <= 65536)
+  int prefix_mmax;     // shared-prefix memo: tiles with U > 0 are allowed when K - U <= prefix_mmax ...
+  int prefix_lmax;     // ... and, for K - U >= 1, when L = N - K + 1 <= prefix_lmax (0 / 0: no memo)
 };
 // Ranks that also have a 16-bit-member-id instantiation (unrolled path; used by
 // plans with n_a <= 65536).
@@ -114,6 +123,10 @@ cudaError_t launch_gather(const double* x, const int32_t* act, double* xa, doubl
 cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, double* xg, int gs, int norm,
                             int64_t n_active, double* ya, cudaStream_t s);
 cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s);
+// shared-prefix group table (prefix.cuh): A and the rows C_i of every group from
+// the series table; gku[g] = k | U << 8
+cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff, double* gtab,
+                          int64_t ngroups, cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)
 cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, int norm, double* partial,

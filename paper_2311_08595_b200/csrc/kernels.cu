@@ -54,6 +54,55 @@ __global__ void series_kernel(const double* __restrict__ xa, double* __restrict_
     series_row(xa[i], xg + i * gs, gs, norm);
 }
 
+// Shared-prefix group table (prefix.cuh), one thread per group: from the
+// normalised series rows of the group's U prefix members, the front
+// A = prod g_j (row format) and, per member i, C_i[j] = A_{\i}[D-j] + A[D-1-j]
+// (unnormalised coefficients; the second term for j <= D-1).  The edge kernel
+// that follows is a programmatic dependent launch (its consumers wait for this
+// grid before reading the table or the series rows).
+__global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
+                             const int64_t* __restrict__ goff, double* __restrict__ gtab, int64_t ngroups) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1, D = L - 1;
+    double* T = gtab + goff[g];
+    const long long* ids = reinterpret_cast<const long long*>(T + L + U * L);
+    double ah[STTSV_MAX_RANK], ai[STTSV_MAX_RANK];
+    double X = 1.0;
+    ah[0] = 1.0;
+    for (int j = 1; j < L; ++j) ah[j] = 0.0;
+    for (int m = 0; m < U; ++m) {  // A = prod of the prefix rows (normalised, leading 1)
+      const double* h = xg + (size_t)ids[m] * gs;
+      for (int j = L - 1; j >= 1; --j) {
+        double s = ah[j] + h[j];
+        for (int i = 1; i < j; ++i) s = fma(ah[i], h[j - i], s);
+        ah[j] = s;
+      }
+      X *= h[0];
+    }
+    T[0] = X;
+    for (int j = 1; j < L; ++j) T[j] = ah[j];
+    for (int i = 0; i < U; ++i) {  // A_{\i}
+      double Xi = 1.0;
+      ai[0] = 1.0;
+      for (int j = 1; j < L; ++j) ai[j] = 0.0;
+      for (int m = 0; m < U; ++m) {
+        if (m == i) continue;
+        const double* h = xg + (size_t)ids[m] * gs;
+        for (int j = L - 1; j >= 1; --j) {
+          double s = ai[j] + h[j];
+          for (int q = 1; q < j; ++q) s = fma(ai[q], h[j - q], s);
+          ai[j] = s;
+        }
+        Xi *= h[0];
+      }
+      double* C = T + L + i * L;
+      for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
+    }
+  }
+}
+
 __global__ void expand_kernel(const double* __restrict__ ya, const int32_t* __restrict__ act,
                               double* __restrict__ y, int64_t n_active) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_active;
@@ -312,6 +361,13 @@ cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, dou
 cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s) {
   if (n_active <= 0) return cudaSuccess;
   series_kernel<<<grid_for(n_active, 256, 4096), 256, 0, s>>>(xa, xg, gs, norm, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff, double* gtab,
+                          int64_t ngroups, cudaStream_t s) {
+  if (ngroups <= 0) return cudaSuccess;
+  group_kernel<<<grid_for(ngroups, 128, 4096), 128, 0, s>>>(xg, gs, N, gku, goff, gtab, ngroups);
   return cudaGetLastError();
 }
 

@@ -201,6 +201,20 @@ static double dp_fma(int N, int k) {
   return f + k + 1;
 }
 
+// FP64 operations per edge with the shared-prefix memo (prefix.cuh) for a tile
+// whose edges share U leading members: M = K - U own members; mirrors
+// dp_front_norm + the SB update + the scalings.  U = 0: dp_fma.
+static double dp_fma_prefix(int N, int k, int U) {
+  if (U == 0) return dp_fma(N, k);
+  const int M = k - U;
+  if (M == 0) return 1.0;  // SB[0] += w'
+  const double L = N - k + 1, D = L - 1, T = L * (L - 1) / 2;
+  double f;
+  if (M == 1) f = (D >= 1 ? D - 1 + 2 : 0) + 1;
+  else f = (M - 2) * (T + 1) + 2 * D + 4 + T + 1 + (D >= 1 ? D - 1 + 2 : 0) + (M - 2) * (D + 3 + T);
+  return f + (L + 1) + 1 + M;
+}
+
 // ------------------------------------------------------------------- plans
 struct sttsv_plan_s {
   int device = 0;
@@ -250,6 +264,9 @@ struct sttsv_plan_s {
   int64_t stream_bytes = 0;
   double fma = 0;
   int64_t allreduces = 0;  // ncclAllReduce calls issued (sttsv_plan_info)
+  double fma_exec = 0;      // FP64 operations the kernel executes per apply (shared-prefix memo counted)
+  const int32_t* d_gku = nullptr;  // per prefix group: k | U << 8 (group_kernel)
+  int64_t prefix_tiles = 0, prefix_groups = 0, prefix_inc = 0;
   // edge-kernel timing (sttsv_plan_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
@@ -343,7 +360,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (world < 1 || rank < 0 || rank >= world) return fail(STTSV_ERR_INVALID_ARGUMENT, "bad world/rank");
   if (comm && (comm->world != world || comm->rank != rank || comm->device != device))
     return fail(STTSV_ERR_INVALID_ARGUMENT, "comm world/rank/device differ from the plan's");
-  const uint32_t known = STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES | STTSV_DETERMINISTIC | STTSV_BATCH_FUSED;
+  const uint32_t known =
+      STTSV_CANONICALIZE | STTSV_MERGE_DUPLICATES | STTSV_DETERMINISTIC | STTSV_BATCH_FUSED | STTSV_NO_PREFIX_MEMO;
   if (flags & ~known) return fail(STTSV_ERR_UNSUPPORTED, "flags 0x%x not implemented in this build", flags & ~known);
 
   // ---- validate; offsets
@@ -466,6 +484,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     const long double w = weights ? (long double)weights[e] : (long double)k;
     wrow[w_off[k] + le] = (double)(w * Ckl[k]);
   }
+  std::vector<std::vector<uint8_t>> tile_u(N + 1);
+  const bool memo = p->ent.prefix_mmax > 0 && !(flags & (STTSV_DETERMINISTIC | STTSV_NO_PREFIX_MEMO)) &&
+                    !getenv("STTSV_NO_PREFIX");
   // Sort each bucket lexicographically (stable: the plan is deterministic).
   // Consecutive edges then share their hot low slots, which the kernel's
   // per-lane run accumulators turn into one deposit per run.
@@ -515,6 +536,21 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = col[(int64_t)i * st + kept - 1];
       h_w[w_off[k] + j] = 0.0;
     }
+    // shared-prefix memo (prefix.cuh): per tile, the number U of leading members
+    // all its edges share = the common prefix of its first and last (sorted) edge
+    const int64_t ntl = padded / tile;
+    tile_u[k].assign(ntl, 0);
+    if (memo) {
+      const int L = N - k + 1;
+      for (int64_t tl = 0; tl < ntl; ++tl) {
+        const int64_t j0 = tl * tile, j1 = j0 + tile - 1;
+        int u = 0;
+        while (u < k && col[(int64_t)u * st + j0] == col[(int64_t)u * st + j1]) ++u;
+        const int M = k - u;
+        const bool ok = u >= 1 && (M == 0 || (M <= p->ent.prefix_mmax && L <= p->ent.prefix_lmax));
+        tile_u[k][tl] = (uint8_t)(ok ? u : 0);
+      }
+    }
   }
   std::vector<int32_t>().swap(rows);
   std::vector<double>().swap(wrow);
@@ -558,9 +594,63 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     fma += dp_fma(N, k) * (double)stored[k];
     p->stored_edges += stored[k];
     p->stored_inc += stored[k] * k;
-    p->stream_bytes += (stored[k] + tile - 1) / tile * tile * (idb * k + 8);
+    const int64_t ntl = (stored[k] + tile - 1) / tile;
+    for (int64_t tl = 0; tl < ntl; ++tl) {
+      const int u = tile_u[k][tl];
+      const int64_t real = std::min<int64_t>(tile, stored[k] - tl * tile);  // edges of the tile that are not padding
+      p->stream_bytes += (int64_t)tile * (idb * (k - u) + 8);
+      p->fma_exec += dp_fma_prefix(N, k, u) * (double)real;
+      if (u > 0) {
+        p->prefix_tiles += 1;
+        p->prefix_inc += (int64_t)u * real;
+      }
+    }
   }
   kp.num_tiles = tiles;
+  // shared-prefix groups: consecutive tiles (kernel order) with the same bucket, U and
+  // prefix ids share a group id; U = 0 tiles have none (-1)
+  std::vector<uint8_t> h_tu;
+  std::vector<int32_t> h_tg, h_gku;
+  std::vector<int64_t> h_goff;
+  std::vector<double> h_gtab;  // group records (prefix.cuh): [A: L][C: U x L][ids: U]; ids filled here
+  if (memo && p->prefix_tiles > 0) {
+    h_tu.resize(tiles);
+    h_tg.resize(tiles);
+    int32_t gid = -1;
+    int pk = -1, pu = -1;
+    std::vector<int32_t> pref, cur;
+    for (int i = 0; i < kp.nb; ++i) {
+      const int k = kp.b[i].k;
+      const int32_t* col = h_ids.data() + ids_off[k];
+      const int64_t ntl = (stored[k] + tile - 1) / tile;
+      for (int64_t tl = 0; tl < ntl; ++tl) {
+        const int64_t t = kp.b[i].tile_begin + tl;
+        const int u = tile_u[k][tl];
+        h_tu[t] = (uint8_t)u;
+        if (u == 0) {
+          h_tg[t] = -1;
+          pk = -1;
+          continue;
+        }
+        cur.assign(u, 0);
+        for (int q = 0; q < u; ++q) cur[q] = col[(int64_t)q * stride[k] + tl * tile];
+        if (!(k == pk && u == pu && cur == pref)) {
+          ++gid;
+          pk = k;
+          pu = u;
+          pref = cur;
+          const int L = N - k + 1;
+          h_gku.push_back(k | (u << 8));
+          h_goff.push_back((int64_t)h_gtab.size());
+          h_gtab.resize(h_gtab.size() + L + (size_t)u * L + u, 0.0);
+          long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - u);
+          for (int q = 0; q < u; ++q) ids[q] = cur[q];
+        }
+        h_tg[t] = gid;
+      }
+    }
+    p->prefix_groups = (int64_t)gid + 1;
+  }
   kp.n_active = (int32_t)na;
   kp.T = T;
   kp.H = H;
@@ -669,7 +759,10 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   const size_t b_xg = align((size_t)na * gs * 8 + 16);
   const size_t b_cta = align(8);
   const size_t b_priv = align((size_t)grid * H * 8 + 8);
-  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv;
+  const size_t b_tu = align(h_tu.size() + 1), b_tg = align(h_tg.size() * 4 + 4);
+  const size_t b_gku = align(h_gku.size() * 4 + 4), b_goff = align(h_goff.size() * 8 + 8),
+               b_gtab = align(h_gtab.size() * 8 + 8);
+  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg + b_gku + b_goff + b_gtab;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -682,6 +775,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->d_xg = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
   unsigned long long* d_cnt = (unsigned long long*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg);
   double* d_priv = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta);
+  uint8_t* d_tu = (uint8_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv);
+  int32_t* d_tg = (int32_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu);
+  char* gbase = base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg;
+  int32_t* d_gku = (int32_t*)gbase;
+  int64_t* d_goff = (int64_t*)(gbase + b_gku);
+  double* d_gtab = (double*)(gbase + b_gku + b_goff);
   p->gs = gs;
   if (ids_total && idb == 4) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ids_total && idb == 2) {
@@ -691,6 +790,16 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   }
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_tu.empty()) ce = cudaMemcpy(d_tu, h_tu.data(), h_tu.size(), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_tg.empty()) ce = cudaMemcpy(d_tg, h_tg.data(), h_tg.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_gku.empty()) ce = cudaMemcpy(d_gku, h_gku.data(), h_gku.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_goff.empty()) ce = cudaMemcpy(d_goff, h_goff.data(), h_goff.size() * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_gtab.empty()) ce = cudaMemcpy(d_gtab, h_gtab.data(), h_gtab.size() * 8, cudaMemcpyHostToDevice);
+  kp.tile_u = h_tu.empty() ? nullptr : d_tu;
+  kp.tile_gid = h_tg.empty() ? nullptr : d_tg;
+  kp.goff = h_goff.empty() ? nullptr : d_goff;
+  kp.gtab = h_gtab.empty() ? nullptr : d_gtab;
+  p->d_gku = d_gku;
   p->h_act = act;
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
   kp.ids = d_ids;
@@ -756,6 +865,11 @@ extern "C" sttsv_status_t sttsv_plan_info(sttsv_plan_t p, sttsv_plan_info_t* inf
   info->kernel_block = p->block;
   info->id_bytes = p->ent.id_bytes;
   info->allreduces = p->allreduces;
+  info->fma_executed = p->fma_exec;
+  info->prefix_tiles = p->prefix_tiles;
+  info->prefix_groups = p->prefix_groups;
+  info->prefix_incidences = p->prefix_inc;
+  info->num_tiles = p->kp.num_tiles;
   return STTSV_OK;
 }
 
@@ -764,6 +878,7 @@ extern "C" int sttsv_apply_launches(sttsv_plan_t p) {
   int l = 0;
   if (p->n_active > 0) l += 2;          // gather + expand
   if (p->kp.num_tiles > 0) l += 1;      // edge kernel
+  if (p->kp.gtab) l += 1;               // shared-prefix group table
   if (p->det) l += 2;                   // deterministic chunk + vertex sums
   return l;
 }
@@ -820,7 +935,11 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
       ev = &p->events[p->events_used++];
       CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
     }
-    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed),
+    const bool groups = p->kp.gtab != nullptr;
+    if (groups)  // per-apply shared-prefix group table (prefix.cuh)
+      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->kp.goff, const_cast<double*>(p->kp.gtab),
+                             p->prefix_groups, s), "group kernel launch");
+    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed || groups),
              "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }
@@ -1062,6 +1181,12 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       kp.ya = p->b_ya;
       kp.ya_vstride = na;
       kp.priv = p->b_priv;
+      // the fused batch pass stages every id column (no shared-prefix memo: the group
+      // table is per vector)
+      kp.tile_u = nullptr;
+      kp.tile_gid = nullptr;
+      kp.goff = nullptr;
+      kp.gtab = nullptr;
       CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0)),
                "edge kernel launch");
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,

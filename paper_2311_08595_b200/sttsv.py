@@ -22,6 +22,7 @@ STTSV_CANONICALIZE = 1 << 0
 STTSV_MERGE_DUPLICATES = 1 << 1
 STTSV_DETERMINISTIC = 1 << 2
 STTSV_BATCH_FUSED = 1 << 3
+STTSV_NO_PREFIX_MEMO = 1 << 4
 
 STATUS = {0: "STTSV_OK", 1: "STTSV_ERR_INVALID_ARGUMENT", 2: "STTSV_ERR_EDGE_SIZE", 3: "STTSV_ERR_VERTEX_RANGE",
           4: "STTSV_ERR_UNSORTED", 5: "STTSV_ERR_REPEATED_VERTEX", 6: "STTSV_ERR_NONFINITE", 7: "STTSV_ERR_ALIAS",
@@ -44,7 +45,9 @@ class PlanInfo(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("stream_bytes", ctypes.c_int64),
                 ("fma_per_apply", ctypes.c_double), ("hot_private", ctypes.c_int32),
                 ("hot_shared", ctypes.c_int32), ("kernel_grid", ctypes.c_int32), ("kernel_block", ctypes.c_int32),
-                ("id_bytes", ctypes.c_int32), ("allreduces", ctypes.c_int64)]
+                ("id_bytes", ctypes.c_int32), ("allreduces", ctypes.c_int64), ("fma_executed", ctypes.c_double),
+                ("prefix_tiles", ctypes.c_int64), ("prefix_groups", ctypes.c_int64),
+                ("prefix_incidences", ctypes.c_int64), ("num_tiles", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "edges_per_size"}
