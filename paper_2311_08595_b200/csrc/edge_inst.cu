@@ -39,6 +39,7 @@ EdgeKernelEntry STTSV_CAT(edge_entry_, STTSV_INST_N)() {
   e.id_bytes = C::IDB;
   e.prefix_mmax = C::PMAX;
   e.prefix_lmax = C::PLMAX;
+  e.red_bytes = (size_t)C::RED_BYTES;
   e.table_norm = ((C::BIG && STTSV_BIG_NORM) || (!C::BIG && STTSV_INST_N >= STTSV_NORM_MIN && STTSV_MID_NORM)) ? 1 : 0;
   return e;
 }

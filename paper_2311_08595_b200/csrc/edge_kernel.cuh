@@ -122,10 +122,15 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #ifndef STTSV_PREFIX_MMAX
 #define STTSV_PREFIX_MMAX 4
 #endif
+#ifndef STTSV_PREFIX_MMAX_BIG
+#define STTSV_PREFIX_MMAX_BIG 8
+#endif
 // suspend-time hint (ns) of the producer's mbarrier waits
 #ifndef STTSV_WAIT_HINT_NS
 #define STTSV_WAIT_HINT_NS 1000000
 #endif
+
+constexpr int kRedStride = 34;  // doubles per row of the prefix reduction area (32 lanes + pad)
 
 // IDB_: bytes per member id in the edge stream (4; or 2 for plans with n_a <=
 // 65536 on the unrolled ranks: 36% fewer stream bytes at mean k = 5)
@@ -138,13 +143,21 @@ struct EdgeCfg {
   static constexpr int EDGE_BYTES = IDB * KMAX + 8;         // staged bytes per edge (ids + w')
   // dynamic shared memory for the TMA ring (<= 227 KB in total; the large-rank
   // path also needs its prefix stack)
-  static constexpr int RING_BUDGET =
-      BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024 : (N <= 10 ? STTSV_RING_KB : 220 / STTSV_MID_BLOCKS) * 1024;
+  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW)
+                                      : (N <= 8 ? STTSV_NCW_SMALL : N <= 10 ? STTSV_NCW_SMALL9 : STTSV_NCW_MID);
+  // shared-prefix memo limits (0: off on this path)
+  static constexpr int PMAX = BIG ? (STTSV_BIG_NORM ? STTSV_PREFIX_MMAX_BIG : 0)
+                                  : ((N < STTSV_NORM_MIN || !STTSV_MID_NORM) ? 0 : STTSV_PREFIX_MMAX);
+  // per consumer warp, LRED rows of kRedStride doubles of shared memory for the
+  // prefix tiles' transpose-reduction of SB (L <= KMAX - 1 terms when M >= 1)
+  static constexpr int LRED = PMAX > 0 && KMAX > 3 ? KMAX - 1 : 0;
+  static constexpr int RED_BYTES = NCW_PREF * LRED * kRedStride * 8;
+  // (the large-rank path runs one CTA per SM: its reduction rows come on top)
+  static constexpr int RING_BUDGET = BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024
+                                         : (N <= 10 ? STTSV_RING_KB : 220 / STTSV_MID_BLOCKS) * 1024 - RED_BYTES;
   // consumer warps per CTA (NCW_PREF), fewer when two stages of the largest
   // bucket would not fit the ring budget
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
-  static constexpr int NCW_PREF = BIG ? (N == 0 && !STTSV_BIG_LOCAL ? 2 : STTSV_BIG_NCW)
-                                      : (N <= 8 ? STTSV_NCW_SMALL : N <= 10 ? STTSV_NCW_SMALL9 : STTSV_NCW_MID);
   static constexpr int NCW = NCW_FIT < NCW_PREF ? (NCW_FIT < 1 ? 1 : NCW_FIT) : NCW_PREF;
   static constexpr int TILE = 32 * NCW * EPL;               // edges per tile
   static constexpr int THREADS = 32 * NCW + 32;             // + one producer warp
@@ -157,9 +170,8 @@ struct EdgeCfg {
   static constexpr int SLOTS = 8;
   static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = BIG ? 1 : (N <= 10 ? STTSV_MIN_BLOCKS : STTSV_MID_BLOCKS);
-  // shared-prefix memo limits (0: off on this path)
-  static constexpr int PMAX = (BIG || N < STTSV_NORM_MIN || !STTSV_MID_NORM) ? 0 : STTSV_PREFIX_MMAX;
-  static constexpr int PLMAX = BIG ? 0 : KMAX;  // (no limit on L on the unrolled path)
+  static constexpr bool BIG_PREFIX = BIG && PMAX > 0;
+  static constexpr int PLMAX = KMAX;  // (no limit on L)
   static_assert(STAGES * STAGE_BYTES <= RING_BUDGET, "ring does not fit");
   static_assert(RING_BYTES >= 2 * STAGE_BYTES, "ring must hold two of the largest stages");
   static_assert(TILE % 4 == 0, "tile must keep 16-byte aligned id columns");
@@ -198,13 +210,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // spinning and stealing issue slots from the consumers
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
+  const uint32_t a = smem_u32(bar);
   for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(STTSV_WAIT_HINT_NS)
+        : "r"(a), "r"(parity), "r"(STTSV_WAIT_HINT_NS)
         : "memory");
     if (ok) return;
   }
@@ -229,6 +242,18 @@ struct Sink {
   double* ya;    // y on active vertices
   int H;
   __device__ __forceinline__ double* at(int v) const { return v < H ? priv + v : ya + v; }
+};
+
+// Weight column of a staged tile: the staged fp64 column, or — buckets whose
+// w' are all equal (plan.cpp; large has w = 1) — the constant for the tile's
+// real edges and 0 for its padding (no weight bytes are streamed).  pos is the
+// edge's sorted position in the tile, col its lane-major column.
+struct WSrc {
+  const double* sw;
+  double wc;
+  int real;  // real (non-padding) edges of the tile (uniform buckets)
+  bool uni;
+  __device__ __forceinline__ double at(int col, int pos) const { return uni ? (pos < real ? wc : 0.0) : sw[col]; }
 };
 
 __device__ __forceinline__ void red_add(double* a, double d) {
@@ -309,7 +334,7 @@ __device__ __forceinline__ void slots_deposit(const int (&id)[K], const double (
 // Buckets are padded to whole tiles with weight-0 copies of their last edge,
 // so every column is valid.
 template <int N, int K, int TILE, int EPL, int RMAX, bool DET, typename IdT>
-__device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const double* __restrict__ sw, int base,
+__device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const WSrc& sw, int base,
                                            const double* __restrict__ xg, RunAcc<RMAX>& ra, const Sink& sk,
                                            const DetSink& ds, int lane) {
   constexpr int L = N - K + 1;
@@ -324,7 +349,7 @@ __device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const d
       id[i] = (int)sids[i * TILE + col];
       rows[i] = xg + (size_t)(uint32_t)id[i] * GS;  // GS compile-time: one IMAD.WIDE.U32
     }
-    const double w = sw[col];
+    const double w = sw.at(col, base + lane * EPL + r);
     double q[K], F;
     if constexpr (N >= STTSV_NORM_MIN && STTSV_MID_NORM) dp_edge_table_norm<K, L>(rows, q, F);
     else dp_edge_table<K, L>(rows, q, F);
@@ -342,7 +367,7 @@ __device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const d
 }
 
 template <int N, int K, int TILE, int EPL, int RMAX, bool DET, typename IdT>
-__device__ __forceinline__ void dispatch_k(int k, const IdT* sids, const double* sw, int base,
+__device__ __forceinline__ void dispatch_k(int k, const IdT* sids, const WSrc& sw, int base,
                                            const double* xg, RunAcc<RMAX>& ra, const Sink& sk, const DetSink& ds,
                                            int lane) {
   if constexpr (K <= N) {
@@ -376,6 +401,63 @@ __device__ __forceinline__ void slots_deposit_off(const int (&id)[M], const doub
   }
 }
 
+// End of a shared-prefix tile (prefix.cuh): sum each of the L terms of the
+// lanes' SB over the warp and deposit the prefix members' totals
+// sum_j C_i[j] T[j] (lane i < U).  L <= 2: shuffle butterfly; else a transpose
+// through this warp's shared-memory rows sred (row j = term j of the 32 lanes,
+// kRedStride apart: conflict-free 16-byte reads).
+template <int L>
+__device__ __forceinline__ void prefix_tile_flush(double (&sb)[L], double* sred, const double* __restrict__ G, int U,
+                                                  const Sink& sk, int lane) {
+  const double* C = G + L;
+  const long long* pid = reinterpret_cast<const long long*>(G + L + U * L);
+  if constexpr (L <= 2) {
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sb[j] += __shfl_xor_sync(kFull, sb[j], o);
+    for (int i = lane; i < U; i += 32) {
+      double c = 0.0;
+#pragma unroll
+      for (int j = 0; j < L; ++j) c = fma(__ldg(C + i * L + j), sb[j], c);
+      red_add(sk.at((int)__ldg(pid + i)), c);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < L; ++j) sred[j * kRedStride + lane] = sb[j];
+    __syncwarp();
+    double t = 0.0;
+    if (lane < L) {
+      const double2* r = reinterpret_cast<const double2*>(sred + lane * kRedStride);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 v = r[q];
+        t += v.x;
+        t += v.y;
+      }
+    }
+    __syncwarp();
+    if (lane < L) sred[lane] = t;
+    __syncwarp();
+    for (int i = lane; i < U; i += 32) {
+      double c = 0.0;
+#pragma unroll
+      for (int j = 0; j < L; ++j) c = fma(__ldg(C + i * L + j), sred[j], c);
+      red_add(sk.at((int)__ldg(pid + i)), c);
+    }
+    __syncwarp();
+  }
+}
+
+// M = 0 tile or edge block (every edge the same vertex set): the prefix members
+// get sum w' times C_i[0]; with uniform weights the sum is wc x (real edges in
+// positions [base, base + n)), no loads at all
+__device__ __forceinline__ void prefix_tile_flush0(double t0, const double* __restrict__ G, int L, int U,
+                                                   const Sink& sk, int lane) {
+  const long long* pid = reinterpret_cast<const long long*>(G + L + U * L);
+  for (int i = lane; i < U; i += 32) red_add(sk.at((int)__ldg(pid + i)), __ldg(G + L + i * L) * t0);
+}
+
 // The warp's block of a staged tile whose edges share their first U = K - M
 // members (the stage holds only the M own id columns).  G: the tile's prefix
 // group in the per-apply group table (prefix.cuh: front A, the contraction
@@ -383,23 +465,32 @@ __device__ __forceinline__ void slots_deposit_off(const int (&id)[M], const doub
 // its edges; at the end of the block the warp sums SB and lane i < U deposits
 // member i's total  sum_j C_i[j] SB[j].
 template <int N, int K, int M, int TILE, int EPL, int RMAX, typename IdT>
-__device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, const double* __restrict__ sw,
+__device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, const WSrc& sw,
                                                   int base, const double* __restrict__ xg,
                                                   const double* __restrict__ G, RunAcc<RMAX>& ra, const Sink& sk,
-                                                  int lane) {
+                                                  double* sred, int lane) {
   constexpr int L = N - K + 1;
   constexpr int GS = series_stride(N);
   constexpr int U = K - M;
-  double sb[L];
-#pragma unroll
-  for (int j = 0; j < L; ++j) sb[j] = 0.0;
   if constexpr (M == 0) {
     // every edge of the tile is the same vertex set: SB = (sum w', 0, ...)
+    double t0;
+    if (sw.uni) {
+      int n = sw.real - base;
+      n = n < 0 ? 0 : (n > 32 * EPL ? 32 * EPL : n);
+      t0 = sw.wc * (double)n;
+    } else {
+      t0 = 0.0;
 #pragma unroll
-    for (int r = 0; r < EPL; ++r) sb[0] += sw[base + r * 32 + lane];
+      for (int r = 0; r < EPL; ++r) t0 += sw.sw[base + r * 32 + lane];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sb[0] += __shfl_xor_sync(kFull, sb[0], o);
+      for (int o = 16; o > 0; o >>= 1) t0 += __shfl_xor_sync(kFull, t0, o);
+    }
+    prefix_tile_flush0(t0, G, L, U, sk, lane);
   } else {
+    double sb[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) sb[j] = 0.0;
     double a[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) a[j] = __ldg(G + j);  // front A (row format), the same on every lane
@@ -413,7 +504,7 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
         id[i] = (int)sids[i * TILE + col];
         load_series<L>(xg + (size_t)(uint32_t)id[i] * GS, h[i]);
       }
-      const double w = sw[col];
+      const double w = sw.at(col, base + lane * EPL + r);
       double q[M], F, bh[L];
       dp_front_norm<M, L>(a, h, q, F, bh);
       const double wF = w * F;
@@ -426,48 +517,34 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
 #pragma unroll
       for (int j = 1; j < L; ++j) sb[j] = fma(c, bh[j], sb[j]);
     }
-#pragma unroll
-    for (int j = 0; j < L; ++j)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sb[j] += __shfl_xor_sync(kFull, sb[j], o);
-  }
-  if (lane < U) {
-    const double* C = G + L + lane * L;
-    double c = 0.0;
-    if constexpr (M == 0) {
-      c = __ldg(C) * sb[0];
-    } else {
-#pragma unroll
-      for (int j = 0; j < L; ++j) c = fma(__ldg(C + j), sb[j], c);
-    }
-    const long long v = __ldg(reinterpret_cast<const long long*>(G + L + U * L) + lane);
-    red_add(sk.at((int)v), c);
+    prefix_tile_flush<L>(sb, sred, G, U, sk, lane);
   }
 }
 
 // prefix tiles of bucket K: dispatch on the number of own members M = K - U
 template <int N, int K, int M, int MMAX, int TILE, int EPL, int RMAX, typename IdT>
-__device__ __forceinline__ void dispatch_m(int m, const IdT* sids, const double* sw, int base, const double* xg,
-                                           const double* G, RunAcc<RMAX>& ra, const Sink& sk, int lane) {
+__device__ __forceinline__ void dispatch_m(int m, const IdT* sids, const WSrc& sw, int base, const double* xg,
+                                           const double* G, RunAcc<RMAX>& ra, const Sink& sk, double* sred,
+                                           int lane) {
   if constexpr (M < K && M <= MMAX) {
     if (m == M) {
-      warp_block_prefix<N, K, M, TILE, EPL, RMAX, IdT>(sids, sw, base, xg, G, ra, sk, lane);
+      warp_block_prefix<N, K, M, TILE, EPL, RMAX, IdT>(sids, sw, base, xg, G, ra, sk, sred, lane);
       return;
     }
-    dispatch_m<N, K, M + 1, MMAX, TILE, EPL, RMAX, IdT>(m, sids, sw, base, xg, G, ra, sk, lane);
+    dispatch_m<N, K, M + 1, MMAX, TILE, EPL, RMAX, IdT>(m, sids, sw, base, xg, G, ra, sk, sred, lane);
   }
 }
 
 template <int N, int K, int MMAX, int TILE, int EPL, int RMAX, typename IdT>
-__device__ __forceinline__ void dispatch_kp(int k, int U, const IdT* sids, const double* sw, int base,
+__device__ __forceinline__ void dispatch_kp(int k, int U, const IdT* sids, const WSrc& sw, int base,
                                             const double* xg, const double* G, RunAcc<RMAX>& ra, const Sink& sk,
-                                            int lane) {
+                                            double* sred, int lane) {
   if constexpr (K <= N) {
     if (k == K) {
-      dispatch_m<N, K, 0, MMAX, TILE, EPL, RMAX, IdT>(K - U, sids, sw, base, xg, G, ra, sk, lane);
+      dispatch_m<N, K, 0, MMAX, TILE, EPL, RMAX, IdT>(K - U, sids, sw, base, xg, G, ra, sk, sred, lane);
       return;
     }
-    dispatch_kp<N, K + 1, MMAX, TILE, EPL, RMAX, IdT>(k, U, sids, sw, base, xg, G, ra, sk, lane);
+    dispatch_kp<N, K + 1, MMAX, TILE, EPL, RMAX, IdT>(k, U, sids, sw, base, xg, G, ra, sk, sred, lane);
   }
 }
 
@@ -721,6 +798,127 @@ __device__ __forceinline__ void dispatch_big(int L_rt, int K, const int32_t* sid
   }
 }
 
+// ---- large-rank path with a shared prefix (prefix.cuh): the lane's edge has U
+// shared leading members (front A, row format a[], from the group table) and M
+// own members (stage columns sid[i * TILE], i < M).  Deposits the own members'
+// contributions (slots U + i) and returns the edge's SB term in sb (+= w' B).
+template <int L, int TILE, int NT, int RB>
+__device__ __forceinline__ void edge_big_front(int M, int U, const int32_t* __restrict__ sid, double w,
+                                               const double (&a)[L], const double* __restrict__ xg, int gs,
+                                               double* __restrict__ stk, RunAcc<RB>& ra, const Sink& sk,
+                                               double (&sb)[L]) {
+  constexpr int D = L - 1;
+  auto row = [&](int i) { return xg + (size_t)(uint32_t)sid[i * TILE] * gs; };  // own member i
+  const double Xa = a[0];
+  if (M == 1) {
+    double h[L];
+    const double x = load_norm<L>(row(0), h);
+    double F = 0.0;
+    if constexpr (D >= 1) F = Xa * x * coef_norm<D - 1, L>(a, h);
+    const double q = D == 0 ? Xa : Xa * a[D];
+    dep_slot<RB>(U, sid[0], w * (q + F), ra, sk);
+    const double c = w * x;
+    sb[0] += c;
+#pragma unroll
+    for (int j = 1; j < L; ++j) sb[j] = fma(c, h[j], sb[j]);
+    return;
+  }
+  // members g'_0 = A, g'_i = own member i - 1 (K' = M + 1)
+  const int KP = M + 1;
+  double cur[L], g[L], S[L];
+#pragma unroll
+  for (int j = 1; j < L; ++j) cur[j] = a[j];
+  double X = Xa;
+#pragma unroll 1
+  for (int i = 1; i <= KP - 3; ++i) {
+    const double xi = load_norm<L>(row(i - 1), g);
+    if (i > 1) {  // P'_0 = A stays in registers, not stacked
+      stk[((i - 1) * L) * NT] = X;
+#pragma unroll
+      for (int j = 1; j < L; ++j) stk[((i - 1) * L + j) * NT] = cur[j];
+    }
+    trunc_mul_norm_inplace<L>(cur, g);
+    X *= xi;
+  }
+  const double xa = load_norm<L>(row(KP - 3), g);
+  const double xb = load_norm<L>(row(KP - 2), S);
+  const double qa = X * xa * coef_norm<D, L>(cur, g);  // own member M-1
+  const double qb = X * xb * coef_norm<D, L>(cur, S);  // own member M-2
+  trunc_mul_norm_inplace<L>(S, g);
+  double Xs = xa * xb;
+  double F = 0.0;
+  if constexpr (D >= 1) F = X * Xs * coef_norm<D - 1, L>(cur, S);
+  const double wF = w * F;
+  dep_slot<RB>(U + M - 1, sid[(M - 1) * TILE], fma(w, qa, wF), ra, sk);
+  dep_slot<RB>(U + M - 2, sid[(M - 2) * TILE], fma(w, qb, wF), ra, sk);
+#pragma unroll 1
+  for (int i = KP - 3; i >= 1; --i) {
+    const double xi = load_norm<L>(row(i - 1), g);
+    double Xp;
+    if (i > 1) {
+      Xp = stk[((i - 1) * L) * NT];
+#pragma unroll
+      for (int j = 1; j < L; ++j) cur[j] = stk[((i - 1) * L + j) * NT];
+    } else {
+      Xp = Xa;
+#pragma unroll
+      for (int j = 1; j < L; ++j) cur[j] = a[j];
+    }
+    dep_slot<RB>(U + i - 1, sid[(i - 1) * TILE], fma(w, Xp * Xs * coef_norm<D, L>(cur, S), wF), ra, sk);
+    trunc_mul_norm_inplace<L>(S, g);  // S'_i = g'_i S'_{i+1}
+    Xs *= xi;
+  }
+  // S = S'_1 = B
+  const double c = w * Xs;
+  sb[0] += c;
+#pragma unroll
+  for (int j = 1; j < L; ++j) sb[j] = fma(c, S[j], sb[j]);
+}
+
+// one warp's 32 edges (lane = column) of a shared-prefix tile on the large-rank path
+template <int L, int TILE, int NT, int RB>
+__device__ __forceinline__ void big_prefix_block(int K, int U, const int32_t* sid, double w, const WSrc& sw, int base,
+                                                 const double* G, const double* xg, int gs, double* stk,
+                                                 RunAcc<RB>& ra, const Sink& sk, double* sred, int lane) {
+  const int M = K - U;
+  if (M == 0) {
+    double t0;
+    if (sw.uni) {
+      int n = sw.real - base;
+      t0 = sw.wc * (double)(n < 0 ? 0 : (n > 32 ? 32 : n));
+    } else {
+      t0 = w;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t0 += __shfl_xor_sync(kFull, t0, o);
+    }
+    prefix_tile_flush0(t0, G, L, U, sk, lane);
+    return;
+  }
+  double sb[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) sb[j] = 0.0;
+  double a[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) a[j] = __ldg(G + j);
+  edge_big_front<L, TILE, NT, RB>(M, U, sid, w, a, xg, gs, stk, ra, sk, sb);
+  prefix_tile_flush<L>(sb, sred, G, U, sk, lane);
+}
+
+template <int L, int LMAX, int TILE, int NT, int RB>
+__device__ __forceinline__ void dispatch_big_prefix(int L_rt, int K, int U, const int32_t* sid, double w,
+                                                    const WSrc& sw, int base, const double* G, const double* xg,
+                                                    int gs, double* stk, RunAcc<RB>& ra, const Sink& sk,
+                                                    double* sred, int lane) {
+  if constexpr (L <= LMAX) {
+    if (L_rt == L) {
+      big_prefix_block<L, TILE, NT, RB>(K, U, sid, w, sw, base, G, xg, gs, stk, ra, sk, sred, lane);
+      return;
+    }
+    dispatch_big_prefix<L + 1, LMAX, TILE, NT, RB>(L_rt, K, U, sid, w, sw, base, G, xg, gs, stk, ra, sk, sred,
+                                                   lane);
+  }
+}
+
 // ------------------------------------------------------------- the kernel
 // N == 0 is the generic instantiation (any rank <= STTSV_MAX_RANK).
 // BATCH = false: one vector (sttsv_apply; runs continue across tiles);
@@ -737,7 +935,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
   // layout: byte ring of stages [ ids k*TILE int32 | w TILE f64 ] | (large-rank path) prefix
   // stacks [p.stack_doubles][NCW*32] f64, thread-interleaved
   unsigned char* ring = smem_raw;
-  double* stack = reinterpret_cast<double*>(smem_raw + Cfg::RING_BYTES);
+  double* sred_all = reinterpret_cast<double*>(smem_raw + Cfg::RING_BYTES);  // prefix reduction rows
+  double* stack = reinterpret_cast<double*>(smem_raw + Cfg::RING_BYTES + Cfg::RED_BYTES);
   // batch (f4): vector v uses xg + v*xg_vstride, ya + v*ya_vstride, priv slice + v*H
   const int nvec = BATCH ? p.nvec : 1;
   double* const priv_cta = p.priv + (size_t)blockIdx.x * p.H * nvec;
@@ -765,27 +964,40 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
     // TILE*(4k+8) bytes carved FIFO out of the byte ring (wrapping to offset 0
     // when the tail of the ring is too short); slot it % SLOTS carries its
     // offset and tile index (published before the mbarrier's release)
-    if (lane == 0) {
-      int b = 0;
-      int64_t ct = 0, ce = 0;
-      uint64_t head = 0, tail = 0;  // ring positions (monotonic; offset = pos % RING_BYTES)
-      uint64_t endpos[SLOTS];       // ring position just past each in-flight slot's stage
-      int64_t oldest = 0;           // oldest iteration whose stage may still be in use
-      for (int64_t it = 0;; ++it) {
-        const int s = (int)(it % SLOTS);
-        if (ct == ce) {
-          // guided: chunks of p.chunk tiles, single tiles once the counter passes
-          // p.guided_from (the tail is split finely across the CTAs)
-          const int64_t want = ct < p.guided_from ? p.chunk : 1;
-          ct = (int64_t)atomicAdd(p.tile_counter, (unsigned long long)want);
-          ce = ct + want < p.num_tiles ? ct + want : p.num_tiles;
-        }
-        const int64_t t = ct < p.num_tiles ? ct++ : -1;
+    // The whole warp loads the packed headers (shared-prefix length U and group
+    // record offset, prefix.cuh) of up to 32 upcoming tiles of its chunk at once, so
+    // lane 0's per-tile path has no dependent global load.
+    __shared__ long long shdr[32];
+    int b = 0;
+    int64_t ct = 0, ce = 0, hb = 0, he = 0;
+    uint64_t head = 0, tail = 0;  // ring positions (monotonic; offset = pos % RING_BYTES), lane 0
+    uint64_t endpos[SLOTS];       // ring position just past each in-flight slot's stage, lane 0
+    int64_t oldest = 0;           // oldest iteration whose stage may still be in use, lane 0
+    for (int64_t it = 0;; ++it) {
+      const int s = (int)(it % SLOTS);
+      if (ct == ce) {
+        // guided: chunks of p.chunk tiles, single tiles once the counter passes
+        // p.guided_from (the tail is split finely across the CTAs)
+        const int64_t want = ct < p.guided_from ? p.chunk : 1;
+        unsigned long long c0 = 0;
+        if (lane == 0) c0 = atomicAdd(p.tile_counter, (unsigned long long)want);
+        ct = (int64_t)__shfl_sync(kFull, c0, 0);
+        ce = ct + want < p.num_tiles ? ct + want : p.num_tiles;
+      }
+      const int64_t t = ct < p.num_tiles ? ct++ : -1;
+      if (t >= 0 && t >= he) {
+        hb = t;
+        he = ce < t + 32 ? ce : t + 32;
+        shdr[lane] = (p.tile_hdr && hb + lane < he) ? __ldg(p.tile_hdr + hb + lane) : 0ll;
+        __syncwarp();
+      }
+      if (lane == 0) {
         if (t >= 0)
           while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
         const int k = t >= 0 ? p.b[b].k : 0;
-        const int tu = (t >= 0 && p.tile_u) ? (int)__ldg(p.tile_u + t) : 0;
-        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (Cfg::IDB * (k - tu) + 8)) : 0u;
+        const long long hdr = t >= 0 ? shdr[t - hb] : 0ll;
+        const int tu = (int)(hdr & 255);
+        const uint32_t need = t >= 0 ? (uint32_t)(TILE * (Cfg::IDB * (k - tu) + (p.b[b].wuni ? 0 : 8))) : 0u;
         uint64_t start = head;
         if (start % Cfg::RING_BYTES + need > (uint64_t)Cfg::RING_BYTES) start += Cfg::RING_BYTES - start % Cfg::RING_BYTES;
         while (it - oldest >= SLOTS || (oldest < it && start + need - tail > (uint64_t)Cfg::RING_BYTES)) {
@@ -800,22 +1012,24 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         soff[s] = off;
         stile[s] = t;
         su[s] = (uint8_t)tu;
-        sgoff[s] = tu > 0 ? __ldg(p.goff + __ldg(p.tile_gid + t)) : 0;
+        sgoff[s] = hdr >> 8;
         if (t < 0) {
           mbar_arrive_expect_tx(&full[s], 0);
-          break;
+        } else {
+          const BucketDesc& bd = p.b[b];
+          const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
+          constexpr uint32_t id_bytes = TILE * Cfg::IDB, w_bytes = TILE * 8;
+          unsigned char* st = ring + off;
+          const unsigned char* idp = reinterpret_cast<const unsigned char*>(p.ids);
+          mbar_arrive_expect_tx(&full[s], need);
+          for (int i = tu; i < k; ++i)  // the shared prefix columns 0..U-1 are not staged
+            bulk_g2s(st + (i - tu) * id_bytes, idp + (size_t)(bd.ids_off + i * bd.stride + e0) * Cfg::IDB, id_bytes,
+                     &full[s]);
+          if (!bd.wuni) bulk_g2s(st + (k - tu) * id_bytes, p.w + bd.w_off + e0, w_bytes, &full[s]);
         }
-        const BucketDesc& bd = p.b[b];
-        const int64_t e0 = (t - bd.tile_begin) * TILE;  // buckets are padded to whole tiles
-        constexpr uint32_t id_bytes = TILE * Cfg::IDB, w_bytes = TILE * 8;
-        unsigned char* st = ring + off;
-        const unsigned char* idp = reinterpret_cast<const unsigned char*>(p.ids);
-        mbar_arrive_expect_tx(&full[s], need);
-        for (int i = tu; i < k; ++i)  // the shared prefix columns 0..U-1 are not staged
-          bulk_g2s(st + (i - tu) * id_bytes, idp + (size_t)(bd.ids_off + i * bd.stride + e0) * Cfg::IDB, id_bytes,
-                   &full[s]);
-        bulk_g2s(st + (k - tu) * id_bytes, p.w + bd.w_off + e0, w_bytes, &full[s]);
       }
+      __syncwarp();
+      if (t < 0) break;
     }
   } else {
     // ---------------- consumer warps
@@ -828,7 +1042,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       ra.rid[i] = -1;  // empty run
       ra.run[i] = 0.0;
     }
-    constexpr bool PREFIX = Cfg::PMAX > 0 && !BATCH && !DET;
+    constexpr bool PREFIX = Cfg::PMAX > 0 && !Cfg::BIG && !BATCH && !DET;
+    double* const sred = sred_all + (Cfg::LRED > 0 ? warp * Cfg::LRED * kRedStride : 0);
     int b = 0;
     bool any = false;
     // programmatic dependent launch: x_a, the series table and y_a are written
@@ -863,13 +1078,16 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         const unsigned char* st = ring + soff[s];
         using IdT = typename std::conditional<Cfg::IDB == 2, uint16_t, int32_t>::type;
         const IdT* sids = reinterpret_cast<const IdT*>(st);
-        const double* sw = reinterpret_cast<const double*>(st + (k - tu) * TILE * Cfg::IDB);
+        const BucketDesc& bdc = p.b[b];
+        const int64_t rem = bdc.m - (t - bdc.tile_begin) * TILE;
+        const WSrc sw{reinterpret_cast<const double*>(st + (k - tu) * TILE * Cfg::IDB), bdc.wc,
+                      (int)(rem < TILE ? rem : TILE), bdc.wuni != 0};
         if constexpr (PREFIX) {
           // shared-prefix tiles (prefix.cuh): the DP over the own members, the
           // prefix members' totals from the group table
           if (tu > 0) {
             dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT>(k, tu, sids, sw, warp * 32 * EPL, p.xg,
-                                                               p.gtab + sgoff[s], ra, sk, lane);
+                                                               p.gtab + sgoff[s], ra, sk, sred, lane);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
             continue;
@@ -884,11 +1102,25 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
             dispatch_k<N, 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xgv, ra, skv, ds, lane);
           } else {
             const int col = warp * 32 + lane;  // EPL = 1
+            if constexpr (Cfg::BIG_PREFIX && !BATCH && !DET) {
+              if (tu > 0) {  // shared-prefix tile (prefix.cuh); warp-uniform
 #if STTSV_BIG_LOCAL
-            dispatch_big<1, KMAX, TILE, 1, RMAX, DET>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs, lstk, ra, skv,
+                dispatch_big_prefix<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col), sw,
+                                                            warp * 32, p.gtab + sgoff[s], xgv, p.gs, lstk, ra, skv,
+                                                            sred, lane);
+#else
+                dispatch_big_prefix<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col),
+                                                                   sw, warp * 32, p.gtab + sgoff[s], xgv, p.gs,
+                                                                   stack + (warp * 32 + lane), ra, skv, sred, lane);
+#endif
+                continue;
+              }
+            }
+#if STTSV_BIG_LOCAL
+            dispatch_big<1, KMAX, TILE, 1, RMAX, DET>(p.N - k + 1, k, sids + col, sw.at(col, col), xgv, p.gs, lstk, ra, skv,
                                                       ds, col);
 #else
-            dispatch_big<1, KMAX, TILE, NCW * 32, RMAX, DET>(p.N - k + 1, k, sids + col, sw[col], xgv, p.gs,
+            dispatch_big<1, KMAX, TILE, NCW * 32, RMAX, DET>(p.N - k + 1, k, sids + col, sw.at(col, col), xgv, p.gs,
                                                              stack + (warp * 32 + lane), ra, skv, ds, col);
 #endif
           }

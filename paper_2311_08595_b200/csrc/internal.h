@@ -14,12 +14,13 @@ namespace sttsv {
 // ascending) of edge e; w[e] = w(e) (N-1)!/|beta(k)| (Alg. 2 factor).
 struct BucketDesc {
   int32_t k;
-  int32_t pad_;
+  int32_t wuni;        // 1: every stored edge has the same w' = wc (no weight column is streamed)
   int64_t m;           // edges in this bucket (this shard)
   int64_t stride;      // column stride of ids: m padded to whole tiles (weight-0 copies of the last edge)
   int64_t tile_begin;  // first tile of this bucket in the kernel's tile order
   int64_t ids_off;     // element offset of column 0 in the ids pool
   int64_t w_off;       // element offset in the weight pool
+  double wc;           // the common w' of a uniform-weight bucket
 };
 
 constexpr int kMaxBuckets = STTSV_MAX_RANK;
@@ -56,12 +57,10 @@ struct EdgeKernelParams {
   unsigned long long* tile_counter;
   int64_t chunk;         // tiles per grab
   int64_t guided_from;   // tile index after which grabs are single tiles
-  // shared-prefix memo (prefix.cuh; nullptr = off): per tile the number U of
-  // leading members all its edges share (their id columns are not streamed) and
-  // its prefix group (-1: U = 0)
-  const uint8_t* tile_u;
-  const int32_t* tile_gid;
-  const int64_t* goff;   // group -> offset of its record in gtab
+  // shared-prefix memo (prefix.cuh; nullptr = off): per tile (goff << 8) | U with
+  // U the number of leading members all its edges share (their id columns are
+  // not streamed) and goff the offset of its prefix group's record in gtab
+  const long long* tile_hdr;
   const double* gtab;    // per-apply group table (prefix.cuh)
 };
 
@@ -86,6 +85,7 @@ struct EdgeKernelEntry {
   int id_bytes;        // bytes per member id in the edge stream (4, or 2: plans with n_a <= 65536)
   int prefix_mmax;     // shared-prefix memo: tiles with U > 0 are allowed when K - U <= prefix_mmax ...
   int prefix_lmax;     // ... and, for K - U >= 1, when L = N - K + 1 <= prefix_lmax (0 / 0: no memo)
+  size_t red_bytes;    // shared memory of the prefix tiles' reduction rows (after the ring)
 };
 // Ranks that also have a 16-bit-member-id instantiation (unrolled path; used by
 // plans with n_a <= 65536).

@@ -54,48 +54,47 @@ __global__ void series_kernel(const double* __restrict__ xa, double* __restrict_
     series_row(xa[i], xg + i * gs, gs, norm);
 }
 
-// Shared-prefix group table (prefix.cuh), one thread per group: from the
-// normalised series rows of the group's U prefix members, the front
-// A = prod g_j (row format) and, per member i, C_i[j] = A_{\i}[D-j] + A[D-1-j]
-// (unnormalised coefficients; the second term for j <= D-1).  The edge kernel
-// that follows is a programmatic dependent launch (its consumers wait for this
-// grid before reading the table or the series rows).
+// Shared-prefix group table (prefix.cuh), one warp per group: lane i < U forms,
+// from the normalised series rows of the group's U prefix members, A_{\i} and
+// A = prod g_j in the same pass and writes C_i[j] = A_{\i}[D-j] + A[D-1-j]
+// (unnormalised coefficients; the second term for j <= D-1); lane 0 also writes
+// the front A (row format).  The edge kernel that follows is a programmatic
+// dependent launch (its consumers wait for this grid before reading the table).
 __global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
                              const int64_t* __restrict__ goff, double* __restrict__ gtab, int64_t ngroups) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
-       g += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < ngroups; g += warps) {
     const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1, D = L - 1;
     double* T = gtab + goff[g];
     const long long* ids = reinterpret_cast<const long long*>(T + L + U * L);
-    double ah[STTSV_MAX_RANK], ai[STTSV_MAX_RANK];
-    double X = 1.0;
-    ah[0] = 1.0;
-    for (int j = 1; j < L; ++j) ah[j] = 0.0;
-    for (int m = 0; m < U; ++m) {  // A = prod of the prefix rows (normalised, leading 1)
-      const double* h = xg + (size_t)ids[m] * gs;
-      for (int j = L - 1; j >= 1; --j) {
-        double s = ah[j] + h[j];
-        for (int i = 1; i < j; ++i) s = fma(ah[i], h[j - i], s);
-        ah[j] = s;
-      }
-      X *= h[0];
-    }
-    T[0] = X;
-    for (int j = 1; j < L; ++j) T[j] = ah[j];
-    for (int i = 0; i < U; ++i) {  // A_{\i}
-      double Xi = 1.0;
-      ai[0] = 1.0;
-      for (int j = 1; j < L; ++j) ai[j] = 0.0;
+    for (int i = lane; i < U; i += 32) {
+      double ah[STTSV_MAX_RANK], ai[STTSV_MAX_RANK];
+      double X = 1.0, Xi = 1.0;
+      ah[0] = ai[0] = 1.0;
+      for (int j = 1; j < L; ++j) ah[j] = ai[j] = 0.0;
       for (int m = 0; m < U; ++m) {
-        if (m == i) continue;
         const double* h = xg + (size_t)ids[m] * gs;
-        for (int j = L - 1; j >= 1; --j) {
-          double s = ai[j] + h[j];
-          for (int q = 1; q < j; ++q) s = fma(ai[q], h[j - q], s);
-          ai[j] = s;
+        const bool in = m != i;
+        for (int j = L - 1; j >= 1; --j) {  // truncated products with implicit leading 1 (descending: in place)
+          const double hj = __ldg(h + j);
+          double s = ah[j] + hj, si = ai[j] + hj;
+          for (int q = 1; q < j; ++q) {
+            const double hq = __ldg(h + j - q);
+            s = fma(ah[q], hq, s);
+            si = fma(ai[q], hq, si);
+          }
+          ah[j] = s;
+          if (in) ai[j] = si;
         }
-        Xi *= h[0];
+        const double x = __ldg(h);
+        X *= x;
+        if (in) Xi *= x;
+      }
+      if (i == 0) {
+        T[0] = X;
+        for (int j = 1; j < L; ++j) T[j] = ah[j];
       }
       double* C = T + L + i * L;
       for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
@@ -306,7 +305,7 @@ EdgeKernelEntry edge_entry(int N, bool id16) {
 int edge_big_stack_doubles(int N) { return big_stack_doubles(N); }
 
 size_t edge_kernel_smem_bytes(const EdgeKernelEntry& e, int N) {
-  return e.ring_bytes + (e.big == 1 ? (size_t)e.consumers * big_stack_doubles(N) * sizeof(double) : 0);
+  return e.ring_bytes + e.red_bytes + (e.big == 1 ? (size_t)e.consumers * big_stack_doubles(N) * sizeof(double) : 0);
 }
 
 cudaError_t edge_kernel_config(const EdgeKernelEntry& e, size_t smem, int* max_blocks_per_sm) {
@@ -367,7 +366,7 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff, double* gtab,
                           int64_t ngroups, cudaStream_t s) {
   if (ngroups <= 0) return cudaSuccess;
-  group_kernel<<<grid_for(ngroups, 128, 4096), 128, 0, s>>>(xg, gs, N, gku, goff, gtab, ngroups);
+  group_kernel<<<grid_for(ngroups * 32, 128, 4096), 128, 0, s>>>(xg, gs, N, gku, goff, gtab, ngroups);
   return cudaGetLastError();
 }
 

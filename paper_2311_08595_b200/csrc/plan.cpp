@@ -266,6 +266,7 @@ struct sttsv_plan_s {
   int64_t allreduces = 0;  // ncclAllReduce calls issued (sttsv_plan_info)
   double fma_exec = 0;      // FP64 operations the kernel executes per apply (shared-prefix memo counted)
   const int32_t* d_gku = nullptr;  // per prefix group: k | U << 8 (group_kernel)
+  const int64_t* d_goff = nullptr;  // per prefix group: offset of its record in the group table
   int64_t prefix_tiles = 0, prefix_groups = 0, prefix_inc = 0;
   // edge-kernel timing (sttsv_plan_profile)
   bool profiling = false;
@@ -485,6 +486,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     wrow[w_off[k] + le] = (double)(w * Ckl[k]);
   }
   std::vector<std::vector<uint8_t>> tile_u(N + 1);
+  std::vector<int> wuni(N + 1, 0);
+  std::vector<double> wconst(N + 1, 0.0);
   const bool memo = p->ent.prefix_mmax > 0 && !(flags & (STTSV_DETERMINISTIC | STTSV_NO_PREFIX_MEMO)) &&
                     !getenv("STTSV_NO_PREFIX");
   // Sort each bucket lexicographically (stable: the plan is deterministic).
@@ -536,6 +539,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       for (int i = 0; i < k; ++i) col[(int64_t)i * st + j] = col[(int64_t)i * st + kept - 1];
       h_w[w_off[k] + j] = 0.0;
     }
+    // uniform weights (e.g. the configs' w = 1): no weight column is streamed; the
+    // kernel uses the constant for real edges and 0 for padding (edge_kernel.cuh WSrc)
+    wuni[k] = memo && kept > 0;
+    for (int64_t j = 1; j < kept && wuni[k]; ++j)
+      if (h_w[w_off[k] + j] != h_w[w_off[k]]) wuni[k] = 0;
+    wconst[k] = kept > 0 ? h_w[w_off[k]] : 0.0;
     // shared-prefix memo (prefix.cuh): per tile, the number U of leading members
     // all its edges share = the common prefix of its first and last (sorted) edge
     const int64_t ntl = padded / tile;
@@ -590,6 +599,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     b.tile_begin = tiles;
     b.ids_off = ids_off[k];
     b.w_off = w_off[k];
+    b.wuni = wuni[k];
+    b.wc = wconst[k];
     tiles += (stored[k] + tile - 1) / tile;
     fma += dp_fma(N, k) * (double)stored[k];
     p->stored_edges += stored[k];
@@ -598,7 +609,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     for (int64_t tl = 0; tl < ntl; ++tl) {
       const int u = tile_u[k][tl];
       const int64_t real = std::min<int64_t>(tile, stored[k] - tl * tile);  // edges of the tile that are not padding
-      p->stream_bytes += (int64_t)tile * (idb * (k - u) + 8);
+      p->stream_bytes += (int64_t)tile * (idb * (k - u) + (wuni[k] ? 0 : 8));
       p->fma_exec += dp_fma_prefix(N, k, u) * (double)real;
       if (u > 0) {
         p->prefix_tiles += 1;
@@ -609,13 +620,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.num_tiles = tiles;
   // shared-prefix groups: consecutive tiles (kernel order) with the same bucket, U and
   // prefix ids share a group id; U = 0 tiles have none (-1)
-  std::vector<uint8_t> h_tu;
-  std::vector<int32_t> h_tg, h_gku;
+  std::vector<long long> h_hdr;  // per tile (goff << 8) | U
+  std::vector<int32_t> h_gku;
   std::vector<int64_t> h_goff;
   std::vector<double> h_gtab;  // group records (prefix.cuh): [A: L][C: U x L][ids: U]; ids filled here
   if (memo && p->prefix_tiles > 0) {
-    h_tu.resize(tiles);
-    h_tg.resize(tiles);
+    h_hdr.assign(tiles, 0);
     int32_t gid = -1;
     int pk = -1, pu = -1;
     std::vector<int32_t> pref, cur;
@@ -626,9 +636,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       for (int64_t tl = 0; tl < ntl; ++tl) {
         const int64_t t = kp.b[i].tile_begin + tl;
         const int u = tile_u[k][tl];
-        h_tu[t] = (uint8_t)u;
         if (u == 0) {
-          h_tg[t] = -1;
           pk = -1;
           continue;
         }
@@ -646,7 +654,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
           long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - u);
           for (int q = 0; q < u; ++q) ids[q] = cur[q];
         }
-        h_tg[t] = gid;
+        h_hdr[t] = ((long long)h_goff[gid] << 8) | u;
       }
     }
     p->prefix_groups = (int64_t)gid + 1;
@@ -759,7 +767,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   const size_t b_xg = align((size_t)na * gs * 8 + 16);
   const size_t b_cta = align(8);
   const size_t b_priv = align((size_t)grid * H * 8 + 8);
-  const size_t b_tu = align(h_tu.size() + 1), b_tg = align(h_tg.size() * 4 + 4);
+  const size_t b_tu = align(h_hdr.size() * 8 + 8), b_tg = 0;
   const size_t b_gku = align(h_gku.size() * 4 + 4), b_goff = align(h_goff.size() * 8 + 8),
                b_gtab = align(h_gtab.size() * 8 + 8);
   p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg + b_gku + b_goff + b_gtab;
@@ -775,8 +783,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->d_xg = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr);
   unsigned long long* d_cnt = (unsigned long long*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg);
   double* d_priv = (double*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta);
-  uint8_t* d_tu = (uint8_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv);
-  int32_t* d_tg = (int32_t*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu);
+  long long* d_hdr = (long long*)(base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv);
   char* gbase = base + b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg;
   int32_t* d_gku = (int32_t*)gbase;
   int64_t* d_goff = (int64_t*)(gbase + b_gku);
@@ -790,16 +797,14 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   }
   if (ce == cudaSuccess && w_total) ce = cudaMemcpy(d_w, h_w.data(), w_total * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && na) ce = cudaMemcpy(p->d_act, act.data(), na * 4, cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess && !h_tu.empty()) ce = cudaMemcpy(d_tu, h_tu.data(), h_tu.size(), cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess && !h_tg.empty()) ce = cudaMemcpy(d_tg, h_tg.data(), h_tg.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_hdr.empty()) ce = cudaMemcpy(d_hdr, h_hdr.data(), h_hdr.size() * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_gku.empty()) ce = cudaMemcpy(d_gku, h_gku.data(), h_gku.size() * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_goff.empty()) ce = cudaMemcpy(d_goff, h_goff.data(), h_goff.size() * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_gtab.empty()) ce = cudaMemcpy(d_gtab, h_gtab.data(), h_gtab.size() * 8, cudaMemcpyHostToDevice);
-  kp.tile_u = h_tu.empty() ? nullptr : d_tu;
-  kp.tile_gid = h_tg.empty() ? nullptr : d_tg;
-  kp.goff = h_goff.empty() ? nullptr : d_goff;
+  kp.tile_hdr = h_hdr.empty() ? nullptr : d_hdr;
   kp.gtab = h_gtab.empty() ? nullptr : d_gtab;
   p->d_gku = d_gku;
+  p->d_goff = d_goff;
   p->h_act = act;
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
   kp.ids = d_ids;
@@ -937,7 +942,7 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
     }
     const bool groups = p->kp.gtab != nullptr;
     if (groups)  // per-apply shared-prefix group table (prefix.cuh)
-      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->kp.goff, const_cast<double*>(p->kp.gtab),
+      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, const_cast<double*>(p->kp.gtab),
                              p->prefix_groups, s), "group kernel launch");
     CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed || groups),
              "edge kernel launch");
@@ -1183,9 +1188,7 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       kp.priv = p->b_priv;
       // the fused batch pass stages every id column (no shared-prefix memo: the group
       // table is per vector)
-      kp.tile_u = nullptr;
-      kp.tile_gid = nullptr;
-      kp.goff = nullptr;
+      kp.tile_hdr = nullptr;
       kp.gtab = nullptr;
       CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0)),
                "edge kernel launch");

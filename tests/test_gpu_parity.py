@@ -531,8 +531,49 @@ def test_id_width(S, torch_cuda, name, m, n, monkeypatch):
         plan = S.Plan.from_hypergraph(hg)
         info = plan.info()
         widths[force32] = info["id_bytes"]
-        assert info["stream_bytes"] >= info["id_bytes"] * info["incidences"] + 8 * info["num_edges"]
+        # shared-prefix columns (prefix.cuh) are not streamed
+        assert info["stream_bytes"] >= (info["id_bytes"] * (info["incidences"] - info["prefix_incidences"])
+                                        + 8 * info["num_edges"])
         assert rel(plan.apply(x).cpu().numpy(), ref) < TOL, (name, force32)
         plan.close()
     expect16 = hg.rank <= 12 and int(np.count_nonzero(np.bincount(hg.indices, minlength=hg.n))) <= 65536
     assert widths[True] == 4 and widths[False] == (2 if expect16 else 4)
+
+
+# ------------------------------------------- shared-prefix memo (f3, prefix.cuh)
+@pytest.mark.parametrize("N,kmax", [(3, 3), (5, 5), (8, 8), (10, 7), (12, 6), (13, 5), (16, 5), (25, 4)])
+def test_prefix_memo(S, torch_cuda, N, kmax):
+    """Edges built in runs that share sorted prefixes of every length 1..k (whole tiles of
+    one repeated set included): the memo plan (default) against the oracle and against the
+    same plan with STTSV_NO_PREFIX_MEMO (every edge's full DP)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(100 + N)
+    n = 400
+    edges = []
+    for _ in range(14 if N <= 12 else 8):
+        k = int(rng.integers(1, kmax + 1))
+        u = int(rng.integers(0, k + 1))
+        pref = sorted(rng.choice(np.arange(0, 40), size=u, replace=False).tolist())
+        rest = [v for v in range(40, n)]
+        cnt = int(rng.integers(500, 4000 if N <= 12 else 1500))
+        for _ in range(cnt):
+            own = rng.choice(rest, size=k - u, replace=False).tolist() if k > u else []
+            edges.append(sorted(pref + own))
+    rng.shuffle(edges)
+    hg = to_hg(n, N, edges, rng.uniform(0.2, 1.5, len(edges)), rng.uniform(0.05, 1.0, n))
+    x = torch.from_numpy(hg.x).cuda()
+    plan = S.Plan.from_hypergraph(hg)
+    info = plan.info()
+    y = plan.apply(x).cpu().numpy()
+    nplan = S.Plan.from_hypergraph(hg, flags=S.STTSV_NO_PREFIX_MEMO)
+    assert nplan.info()["prefix_tiles"] == 0
+    y0 = nplan.apply(x).cpu().numpy()
+    assert info["prefix_tiles"] > 0 and info["prefix_groups"] > 0, info
+    assert rel(y, y0) < TIGHT
+    assert rel(y, oracle.sttsv(hg)) < TOL
+    # the group table is rebuilt every apply: a second x through the same plan
+    x2 = rng.uniform(0.05, 1.0, n)
+    y2 = plan.apply(torch.from_numpy(x2).cuda()).cpu().numpy()
+    assert rel(y2, oracle.sttsv(hg, x=x2)) < TOL
+    plan.close()
+    nplan.close()

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--configs", default="tiny,mid,high-rank,large,centrality")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--quick", action="store_true", help="skip the batch / deterministic / HEC extras")
     args = ap.parse_args()
     hbm, hbm_src = bench.measured_peaks()
     fp64, fp64_src = bench.fp64_peak_tflops()
@@ -78,6 +79,35 @@ def main():
                "stream_hbm_frac": (info["id_bytes"] * info["incidences"] + 8 * info["num_edges"]
                                    + 16 * info["n_active"]) / (kavg * 1e-3) / 1e9 / hbm,
                "peaks": {"hbm_gbs": hbm, "hbm_src": hbm_src, "fp64_tflops": fp64, "fp64_src": fp64_src}}
+        rec["memo"] = {k: info[k] for k in ("fma_executed", "prefix_tiles", "prefix_groups", "prefix_incidences",
+                                           "num_tiles", "stream_bytes")}
+        rec["edge_kernel_fp64_exec_frac"] = 2 * info["fma_executed"] / (kavg * 1e-3) / 1e12 / fp64
+        rec["stream_gbs"] = info["stream_bytes"] / (kavg * 1e-3) / 1e9
+        rec["stream_frac"] = rec["stream_gbs"] / hbm
+        # A/B: the same product without the shared-prefix memo (every edge runs its full DP)
+        nplan = S.Plan.from_hypergraph(hg, flags=S.STTSV_NO_PREFIX_MEMO)
+        y2 = torch.empty_like(x)
+        for _ in range(3):
+            nplan.apply(x, y2)
+        torch.cuda.synchronize()
+        nplan.profile(True)
+        nmed, _ = ev_time(lambda: nplan.apply(x, y2), args.reps, stream)
+        nkms, nkn = nplan.profile_read()
+        nplan.profile(False)
+        rec["no_memo"] = {"apply_ms_median": nmed, "edge_kernel_ms": nkms / max(nkn, 1),
+                          "stream_bytes": nplan.info()["stream_bytes"],
+                          "rel_diff_vs_memo": float(((y2 - y).abs().max() / y.abs().max()).item())}
+        nplan.close()
+        del nplan, y2
+        if args.quick:
+            line = json.dumps(rec)
+            print(line, flush=True)
+            if out:
+                out.write(line + "\n")
+            plan.close()
+            del plan, x, y, hg
+            torch.cuda.empty_cache()
+            continue
         # f4: 4 vectors, one pass per vector (default) and one fused pass (STTSV_BATCH_FUSED)
         X = x.unsqueeze(0).repeat(4, 1)
         Y = torch.empty_like(X)
