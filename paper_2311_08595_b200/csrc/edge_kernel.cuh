@@ -167,7 +167,7 @@ struct EdgeCfg {
   // byte ring: a stage takes TILE*(4k+8) bytes of its bucket's k, so small-k
   // tiles are more deep in flight; SLOTS bounds the stages in flight
   static constexpr int RING_BYTES = (STAGES * STAGE_BYTES > RING_BUDGET ? STAGES * STAGE_BYTES : RING_BUDGET) / 128 * 128;
-  static constexpr int SLOTS = 8;
+  static constexpr int SLOTS = 16;
   static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = BIG ? 1 : (N <= 10 ? STTSV_MIN_BLOCKS : STTSV_MID_BLOCKS);
   static constexpr bool BIG_PREFIX = BIG && PMAX > 0;
@@ -948,6 +948,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
   __shared__ int64_t stile[SLOTS];  // tile index staged in each slot (-1: no more work)
   __shared__ int64_t sgoff[SLOTS];  // its prefix group's offset in the group table ...
   __shared__ uint8_t su[SLOTS];     // ... and shared-prefix length U (its first U id columns are not staged)
+  __shared__ uint8_t sbk[SLOTS];    // its bucket (index into p.b)
 
   for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) priv_cta[j] = 0.0;
   if (tid == 0) {
@@ -1012,6 +1013,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         soff[s] = off;
         stile[s] = t;
         su[s] = (uint8_t)tu;
+        sbk[s] = (uint8_t)b;
         sgoff[s] = hdr >> 8;
         if (t < 0) {
           mbar_arrive_expect_tx(&full[s], 0);
@@ -1042,10 +1044,23 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       ra.rid[i] = -1;  // empty run
       ra.run[i] = 0.0;
     }
-    constexpr bool PREFIX = Cfg::PMAX > 0 && !Cfg::BIG && !BATCH && !DET;
+    constexpr bool PREFIX = Cfg::PMAX > 0 && !Cfg::BIG && !DET;
     double* const sred = sred_all + (Cfg::LRED > 0 ? warp * Cfg::LRED * kRedStride : 0);
-    int b = 0;
     bool any = false;
+    // pending M = 0 prefix group (prefix.cuh): consecutive tiles whose edges are all one
+    // vertex set of the same group only add their weights (this lane's share) here;
+    // the group's totals are deposited once, when another M = 0 group starts or at the end
+    int64_t pend_goff = -1;
+    int pend_L = 0, pend_U = 0;
+    double pend_w = 0.0;
+    auto flush_pending = [&]() {
+      double t0 = pend_w;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t0 += __shfl_xor_sync(kFull, t0, o);
+      for (int v = 0; v < nvec; ++v)
+        prefix_tile_flush0(t0, p.gtab + (size_t)v * p.gtab_vstride + pend_goff, pend_L, pend_U,
+                           Sink{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H}, lane);
+    };
     // programmatic dependent launch: x_a, the series table and y_a are written
     // by the prologue grid (no-op when launched without the PDL attribute)
     griddep_wait();
@@ -1066,7 +1081,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       const int64_t t = stile[s];
       if (t < 0) break;
       any = true;
-      while (b + 1 < p.nb && t >= p.b[b + 1].tile_begin) ++b;
+      const int b = sbk[s];
       const int k = p.b[b].k;
 #if STTSV_WAITPROF > 1
       const long long kc0 = clock64();
@@ -1082,12 +1097,29 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         const int64_t rem = bdc.m - (t - bdc.tile_begin) * TILE;
         const WSrc sw{reinterpret_cast<const double*>(st + (k - tu) * TILE * Cfg::IDB), bdc.wc,
                       (int)(rem < TILE ? rem : TILE), bdc.wuni != 0};
-        if constexpr (PREFIX) {
-          // shared-prefix tiles (prefix.cuh): the DP over the own members, the
-          // prefix members' totals from the group table
-          if (tu > 0) {
-            dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT>(k, tu, sids, sw, warp * 32 * EPL, p.xg,
-                                                               p.gtab + sgoff[s], ra, sk, sred, lane);
+        if constexpr (PREFIX || Cfg::BIG_PREFIX) {
+          if (tu > 0 && tu == k && !DET) {
+            // M = 0: every edge of the warp's block is the same vertex set
+            const int nb = Cfg::BIG ? 32 : 32 * EPL;
+            const int bb = Cfg::BIG ? warp * 32 : base;
+            double part = 0.0;
+            if (sw.uni) {
+              int n = sw.real - bb;
+              n = n < 0 ? 0 : (n > nb ? nb : n);
+              part = lane == 0 ? sw.wc * (double)n : 0.0;
+            } else {
+#pragma unroll
+              for (int r = 0; r < (Cfg::BIG ? 1 : EPL); ++r) part += sw.sw[bb + r * 32 + lane];
+            }
+            const int64_t g = sgoff[s];
+            if (g != pend_goff) {
+              if (pend_goff >= 0) flush_pending();
+              pend_goff = g;
+              pend_L = p.N - k + 1;
+              pend_U = tu;
+              pend_w = 0.0;
+            }
+            pend_w += part;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
             continue;
@@ -1098,31 +1130,43 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         for (int v = 0; v < nvec; ++v) {
           const Sink skv{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H};
           const double* xgv = p.xg + (size_t)v * p.xg_vstride;
+          // shared-prefix tiles (prefix.cuh): the DP over the own members, the
+          // prefix members' totals from the vector's group table
+          const double* Gv = p.gtab + (size_t)v * p.gtab_vstride + sgoff[s];
+          bool done = false;
           if constexpr (!Cfg::BIG) {
-            dispatch_k<N, 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xgv, ra, skv, ds, lane);
+            if constexpr (PREFIX) {
+              if (tu > 0) {
+                dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT>(k, tu, sids, sw, base, xgv, Gv, ra, skv, sred,
+                                                                   lane);
+                done = true;
+              }
+            }
+            if (!done) dispatch_k<N, 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xgv, ra, skv, ds, lane);
           } else {
             const int col = warp * 32 + lane;  // EPL = 1
-            if constexpr (Cfg::BIG_PREFIX && !BATCH && !DET) {
+            if constexpr (Cfg::BIG_PREFIX && !DET) {
               if (tu > 0) {  // shared-prefix tile (prefix.cuh); warp-uniform
 #if STTSV_BIG_LOCAL
                 dispatch_big_prefix<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col), sw,
-                                                            warp * 32, p.gtab + sgoff[s], xgv, p.gs, lstk, ra, skv,
-                                                            sred, lane);
+                                                            warp * 32, Gv, xgv, p.gs, lstk, ra, skv, sred, lane);
 #else
                 dispatch_big_prefix<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col),
-                                                                   sw, warp * 32, p.gtab + sgoff[s], xgv, p.gs,
+                                                                   sw, warp * 32, Gv, xgv, p.gs,
                                                                    stack + (warp * 32 + lane), ra, skv, sred, lane);
 #endif
-                continue;
+                done = true;
               }
             }
+            if (!done) {
 #if STTSV_BIG_LOCAL
-            dispatch_big<1, KMAX, TILE, 1, RMAX, DET>(p.N - k + 1, k, sids + col, sw.at(col, col), xgv, p.gs, lstk, ra, skv,
-                                                      ds, col);
+              dispatch_big<1, KMAX, TILE, 1, RMAX, DET>(p.N - k + 1, k, sids + col, sw.at(col, col), xgv, p.gs, lstk,
+                                                        ra, skv, ds, col);
 #else
-            dispatch_big<1, KMAX, TILE, NCW * 32, RMAX, DET>(p.N - k + 1, k, sids + col, sw.at(col, col), xgv, p.gs,
-                                                             stack + (warp * 32 + lane), ra, skv, ds, col);
+              dispatch_big<1, KMAX, TILE, NCW * 32, RMAX, DET>(p.N - k + 1, k, sids + col, sw.at(col, col), xgv,
+                                                               p.gs, stack + (warp * 32 + lane), ra, skv, ds, col);
 #endif
+            }
           }
           if constexpr (BATCH) {
 #pragma unroll
@@ -1150,6 +1194,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       atomicAdd(&g_wait_cycles[2], 1ull);
     }
 #endif
+    if (pend_goff >= 0) flush_pending();
     // flush the run accumulators (single-vector mode)
     if (any && !BATCH) {
 #pragma unroll

@@ -61,14 +61,17 @@ __global__ void series_kernel(const double* __restrict__ xa, double* __restrict_
 // the front A (row format).  The edge kernel that follows is a programmatic
 // dependent launch (its consumers wait for this grid before reading the table).
 __global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
-                             const int64_t* __restrict__ goff, double* __restrict__ gtab, int64_t ngroups) {
+                             const int64_t* __restrict__ goff, const double* gtab_in, double* gtab,
+                             int64_t ngroups) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < ngroups; g += warps) {
     const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1, D = L - 1;
     double* T = gtab + goff[g];
-    const long long* ids = reinterpret_cast<const long long*>(T + L + U * L);
+    const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
+    if (gtab_in != gtab)  // a batch vector's copy of the table: carry the prefix ids over
+      for (int i = lane; i < U; i += 32) reinterpret_cast<long long*>(T + L + U * L)[i] = ids[i];
     for (int i = lane; i < U; i += 32) {
       double ah[STTSV_MAX_RANK], ai[STTSV_MAX_RANK];
       double X = 1.0, Xi = 1.0;
@@ -363,10 +366,10 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
   return cudaGetLastError();
 }
 
-cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff, double* gtab,
-                          int64_t ngroups, cudaStream_t s) {
+cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
+                          const double* gtab_in, double* gtab_out, int64_t ngroups, cudaStream_t s) {
   if (ngroups <= 0) return cudaSuccess;
-  group_kernel<<<grid_for(ngroups * 32, 128, 4096), 128, 0, s>>>(xg, gs, N, gku, goff, gtab, ngroups);
+  group_kernel<<<grid_for(ngroups * 32, 128, 4096), 128, 0, s>>>(xg, gs, N, gku, goff, gtab_in, gtab_out, ngroups);
   return cudaGetLastError();
 }
 

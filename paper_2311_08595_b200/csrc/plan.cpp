@@ -255,7 +255,8 @@ struct sttsv_plan_s {
   // batch (f4) workspace, grown on demand by sttsv_apply_batch
   int batch_cap = 0;
   void* batch_mem = nullptr;
-  double *b_xa = nullptr, *b_xg = nullptr, *b_ya = nullptr, *b_priv = nullptr;
+  double *b_xa = nullptr, *b_xg = nullptr, *b_ya = nullptr, *b_priv = nullptr, *b_gtab = nullptr;
+  int64_t gtab_doubles = 0;  // size of the group table (prefix.cuh)
   // kernel
   EdgeKernelEntry ent{};
   EdgeKernelParams kp{};
@@ -803,6 +804,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (ce == cudaSuccess && !h_gtab.empty()) ce = cudaMemcpy(d_gtab, h_gtab.data(), h_gtab.size() * 8, cudaMemcpyHostToDevice);
   kp.tile_hdr = h_hdr.empty() ? nullptr : d_hdr;
   kp.gtab = h_gtab.empty() ? nullptr : d_gtab;
+  kp.gtab_vstride = 0;
+  p->gtab_doubles = (int64_t)h_gtab.size();
   p->d_gku = d_gku;
   p->d_goff = d_goff;
   p->h_act = act;
@@ -942,7 +945,7 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
     }
     const bool groups = p->kp.gtab != nullptr;
     if (groups)  // per-apply shared-prefix group table (prefix.cuh)
-      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, const_cast<double*>(p->kp.gtab),
+      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->kp.gtab, const_cast<double*>(p->kp.gtab),
                              p->prefix_groups, s), "group kernel launch");
     CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed || groups),
              "edge kernel launch");
@@ -1163,13 +1166,15 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
     p->batch_cap = 0;
     const size_t a = ((size_t)nvec * na * 8 + 255) & ~(size_t)255;
     const size_t gbytes = ((size_t)nvec * na * p->gs * 8 + 255) & ~(size_t)255;
-    const size_t pr = (size_t)p->grid * p->kp.H * nvec * 8 + 8;
-    CUDA_TRY(cudaMalloc(&p->batch_mem, 2 * a + gbytes + pr), "cudaMalloc batch workspace");
+    const size_t pr = ((size_t)p->grid * p->kp.H * nvec * 8 + 8 + 255) & ~(size_t)255;
+    const size_t gt = (size_t)nvec * p->gtab_doubles * 8 + 8;  // per-vector group tables (prefix.cuh)
+    CUDA_TRY(cudaMalloc(&p->batch_mem, 2 * a + gbytes + pr + gt), "cudaMalloc batch workspace");
     char* b = (char*)p->batch_mem;
     p->b_xa = (double*)b;
     p->b_ya = (double*)(b + a);
     p->b_xg = (double*)(b + 2 * a);
     p->b_priv = (double*)(b + 2 * a + gbytes);
+    p->b_gtab = (double*)(b + 2 * a + gbytes + pr);
     p->batch_cap = nvec;
   }
   for (int v = 0; v < nvec; ++v)
@@ -1186,11 +1191,16 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       kp.ya = p->b_ya;
       kp.ya_vstride = na;
       kp.priv = p->b_priv;
-      // the fused batch pass stages every id column (no shared-prefix memo: the group
-      // table is per vector)
-      kp.tile_hdr = nullptr;
-      kp.gtab = nullptr;
-      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0)),
+      // shared-prefix memo: one group table per vector (prefix.cuh)
+      const bool groups = p->kp.gtab != nullptr;
+      if (groups) {
+        for (int v = 0; v < nvec; ++v)
+          CUDA_TRY(launch_groups(p->b_xg + (size_t)v * na * p->gs, p->gs, p->N, p->d_gku, p->d_goff, p->kp.gtab,
+                                 p->b_gtab + (size_t)v * p->gtab_doubles, p->prefix_groups, s), "group kernel launch");
+        kp.gtab = p->b_gtab;
+        kp.gtab_vstride = p->gtab_doubles;
+      }
+      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0), groups),
                "edge kernel launch");
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,
                                              p->b_ya, na, s), "deterministic reduce launch");
