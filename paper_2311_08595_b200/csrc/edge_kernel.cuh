@@ -151,7 +151,12 @@ struct EdgeCfg {
   // per consumer warp, LRED rows of kRedStride doubles of shared memory for the
   // prefix tiles' transpose-reduction of SB (L <= KMAX - 1 terms when M >= 1)
   static constexpr int LRED = PMAX > 0 && KMAX > 3 ? KMAX - 1 : 0;
-  static constexpr int RED_BYTES = NCW_PREF * LRED * kRedStride * 8;
+  // per-warp scratch: the reduction rows, or (unrolled path) the run queue of a
+  // block (32*EPL entries of (sum w', column): 12 bytes each)
+  static constexpr int EPL_ = BIG ? 1 : (IDB == 2 ? STTSV_EPL16 : STTSV_EPL);
+  static constexpr int QBYTES = (PMAX > 0 && !BIG) ? 32 * EPL_ * 12 : 0;
+  static constexpr int SCR_DOUBLES = ((LRED * kRedStride * 8 > QBYTES ? LRED * kRedStride * 8 : QBYTES) + 15) / 16 * 2;
+  static constexpr int RED_BYTES = NCW_PREF * SCR_DOUBLES * 8;
   // (the large-rank path runs one CTA per SM: its reduction rows come on top)
   static constexpr int RING_BUDGET = BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024
                                          : (N <= 10 ? STTSV_RING_KB : 220 / STTSV_MID_BLOCKS) * 1024 - RED_BYTES;
@@ -494,9 +499,71 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
     double a[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) a[j] = __ldg(G + j);  // front A (row format), the same on every lane
-#pragma unroll 1
+    // Runs of identical consecutive edges among the lane's EPL edges (sorted
+    // buckets keep duplicates adjacent) need one DP each, on the run's summed
+    // weight: pass 1 counts the lane's runs, a warp scan places them in this
+    // warp's queue (scratch sred), pass 2 writes (sum w', column) per run; then
+    // the warp works through the queue, lane l taking entries l*c .. l*c+c-1
+    // (consecutive distinct edges: the deposit runs carry over).
+    double* qw = sred;
+    int* qc = reinterpret_cast<int*>(sred + 32 * EPL);
+    int prev[M];
+    int nrun = 0;
+#pragma unroll
     for (int r = 0; r < EPL; ++r) {
       const int col = base + r * 32 + lane;
+      bool same = r > 0;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int v = (int)sids[i * TILE + col];
+        same = same && v == prev[i];
+        prev[i] = v;
+      }
+      nrun += same ? 0 : 1;
+    }
+    int incl = nrun;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int Q = __shfl_sync(kFull, incl, 31);
+    {
+      int pos = incl - nrun, rc = -1;
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < EPL; ++r) {
+        const int col = base + r * 32 + lane;
+        bool same = r > 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          const int v = (int)sids[i * TILE + col];
+          same = same && v == prev[i];
+          prev[i] = v;
+        }
+        const double w = sw.at(col, base + lane * EPL + r);
+        if (!same) {
+          if (rc >= 0) {
+            qw[pos] = acc;
+            qc[pos] = rc;
+            ++pos;
+          }
+          rc = col;
+          acc = w;
+        } else {
+          acc += w;
+        }
+      }
+      qw[pos] = acc;
+      qc[pos] = rc;
+    }
+    __syncwarp();
+    const int c = (Q + 31) >> 5;
+#pragma unroll 1
+    for (int e = lane * c; e < lane * c + c; ++e) {
+      const bool live = e < Q;
+      const int col = qc[live ? e : 0];
+      const double w = live ? qw[e] : 0.0;
       int id[M];
       double h[M][L];
 #pragma unroll
@@ -504,19 +571,19 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
         id[i] = (int)sids[i * TILE + col];
         load_series<L>(xg + (size_t)(uint32_t)id[i] * GS, h[i]);
       }
-      const double w = sw.at(col, base + lane * EPL + r);
       double q[M], F, bh[L];
       dp_front_norm<M, L>(a, h, q, F, bh);
       const double wF = w * F;
       double dv[M];
 #pragma unroll
       for (int i = 0; i < M; ++i) dv[i] = fma(w, q[i], wF);
-      slots_deposit_off<M, U, RMAX>(id, dv, ra, sk);
-      const double c = w * bh[0];
-      sb[0] += c;
+      if (live) slots_deposit_off<M, U, RMAX>(id, dv, ra, sk);
+      const double cw = w * bh[0];
+      sb[0] += cw;
 #pragma unroll
-      for (int j = 1; j < L; ++j) sb[j] = fma(c, bh[j], sb[j]);
+      for (int j = 1; j < L; ++j) sb[j] = fma(cw, bh[j], sb[j]);
     }
+    __syncwarp();  // the queue is read before the reduction reuses the scratch
     prefix_tile_flush<L>(sb, sred, G, U, sk, lane);
   }
 }
@@ -1045,7 +1112,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       ra.run[i] = 0.0;
     }
     constexpr bool PREFIX = Cfg::PMAX > 0 && !Cfg::BIG && !DET;
-    double* const sred = sred_all + (Cfg::LRED > 0 ? warp * Cfg::LRED * kRedStride : 0);
+    double* const sred = sred_all + warp * Cfg::SCR_DOUBLES;
     bool any = false;
     // pending M = 0 prefix group (prefix.cuh): consecutive tiles whose edges are all one
     // vertex set of the same group only add their weights (this lane's share) here;
