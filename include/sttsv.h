@@ -213,8 +213,9 @@ typedef struct {
   int64_t allreduces;      /* ncclAllReduce calls this plan has issued (0 without a comm) */
   double  fma_executed;    /* FP64 operations the edge kernel executes per apply: fma_per_apply minus
                               what the shared-prefix memo saves                 */
-  int64_t prefix_tiles;    /* tiles whose edges share a member prefix (its id columns are not streamed) */
-  int64_t prefix_groups;   /* runs of consecutive such tiles with the same prefix                  */
+  int64_t prefix_tiles;    /* warp blocks (num_tiles x consumer warps in all) whose edges share a member
+                              prefix; the columns every block of a tile shares are not streamed    */
+  int64_t prefix_groups;   /* runs of consecutive such blocks with the same prefix                 */
   int64_t prefix_incidences; /* incidences that lie in a shared prefix                            */
   int64_t num_tiles;       /* tiles of the edge stream                                            */
 } sttsv_plan_info_t;

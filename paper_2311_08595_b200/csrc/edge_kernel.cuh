@@ -213,7 +213,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // producer-side wait: try_wait with a suspend-time hint, so the waiting thread
 // sleeps in hardware until the phase completes (or the hint expires) instead of
 // spinning and stealing issue slots from the consumers
+#ifndef STTSV_PRODUCER_SPIN
+#define STTSV_PRODUCER_SPIN 0
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#if STTSV_PRODUCER_SPIN
+  mbar_wait(bar, parity);
+  return;
+#endif
   uint32_t ok = 0;
   const uint32_t a = smem_u32(bar);
   for (;;) {
@@ -1013,8 +1020,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
   __shared__ uint32_t soff[SLOTS];  // byte offset of each slot's stage in the ring
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int64_t stile[SLOTS];  // tile index staged in each slot (-1: no more work)
-  __shared__ int64_t sgoff[SLOTS];  // its prefix group's offset in the group table ...
-  __shared__ uint8_t su[SLOTS];     // ... and shared-prefix length U (its first U id columns are not staged)
+  __shared__ uint8_t su[SLOTS];     // its staged prefix length U_stage (id columns 0..U_stage-1 are not staged)
+  __shared__ long long sblk[SLOTS][NCW];  // per warp block: (group record offset << 8) | U (prefix.cuh)
   __shared__ uint8_t sbk[SLOTS];    // its bucket (index into p.b)
 
   for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) priv_cta[j] = 0.0;
@@ -1036,6 +1043,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
     // record offset, prefix.cuh) of up to 32 upcoming tiles of its chunk at once, so
     // lane 0's per-tile path has no dependent global load.
     __shared__ long long shdr[32];
+    __shared__ long long shblk[32][NCW];
     int b = 0;
     int64_t ct = 0, ce = 0, hb = 0, he = 0;
     uint64_t head = 0, tail = 0;  // ring positions (monotonic; offset = pos % RING_BYTES), lane 0
@@ -1056,7 +1064,11 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       if (t >= 0 && t >= he) {
         hb = t;
         he = ce < t + 32 ? ce : t + 32;
-        shdr[lane] = (p.tile_hdr && hb + lane < he) ? __ldg(p.tile_hdr + hb + lane) : 0ll;
+        const bool hv = p.tile_hdr && hb + lane < he;
+        const long long* th = p.tile_hdr + (size_t)(hb + lane) * (NCW + 1);
+        shdr[lane] = hv ? __ldg(th) : 0ll;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) shblk[lane][w] = hv ? __ldg(th + 1 + w) : 0ll;
         __syncwarp();
       }
       if (lane == 0) {
@@ -1081,7 +1093,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         stile[s] = t;
         su[s] = (uint8_t)tu;
         sbk[s] = (uint8_t)b;
-        sgoff[s] = hdr >> 8;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) sblk[s][w] = t >= 0 ? shblk[t - hb][w] : 0ll;
         if (t < 0) {
           mbar_arrive_expect_tx(&full[s], 0);
         } else {
@@ -1155,14 +1168,18 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
 #endif
       const DetSink ds{DET ? p.slot + p.b[b].ids_off + (t - p.b[b].tile_begin) * TILE : nullptr, p.b[b].stride,
                        p.contrib};
-      const int tu = su[s];
+      const int us = su[s];                 // staged from column us
+      const long long bh = sblk[s][warp];   // this warp's block: shared prefix length and group
+      const int tu = (int)(bh & 255);
+      const int64_t goff = bh >> 8;
       {
         const unsigned char* st = ring + soff[s];
         using IdT = typename std::conditional<Cfg::IDB == 2, uint16_t, int32_t>::type;
-        const IdT* sids = reinterpret_cast<const IdT*>(st);
+        // the warp's own id columns (slots tu..k-1) start at stage column tu - us
+        const IdT* sids = reinterpret_cast<const IdT*>(st) + (size_t)(tu - us) * TILE;
         const BucketDesc& bdc = p.b[b];
         const int64_t rem = bdc.m - (t - bdc.tile_begin) * TILE;
-        const WSrc sw{reinterpret_cast<const double*>(st + (k - tu) * TILE * Cfg::IDB), bdc.wc,
+        const WSrc sw{reinterpret_cast<const double*>(st + (k - us) * TILE * Cfg::IDB), bdc.wc,
                       (int)(rem < TILE ? rem : TILE), bdc.wuni != 0};
         if constexpr (PREFIX || Cfg::BIG_PREFIX) {
           if (tu > 0 && tu == k && !DET) {
@@ -1178,7 +1195,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
 #pragma unroll
               for (int r = 0; r < (Cfg::BIG ? 1 : EPL); ++r) part += sw.sw[bb + r * 32 + lane];
             }
-            const int64_t g = sgoff[s];
+            const int64_t g = goff;
             if (g != pend_goff) {
               if (pend_goff >= 0) flush_pending();
               pend_goff = g;
@@ -1199,7 +1216,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
           const double* xgv = p.xg + (size_t)v * p.xg_vstride;
           // shared-prefix tiles (prefix.cuh): the DP over the own members, the
           // prefix members' totals from the vector's group table
-          const double* Gv = p.gtab + (size_t)v * p.gtab_vstride + sgoff[s];
+          const double* Gv = p.gtab + (size_t)v * p.gtab_vstride + goff;
           bool done = false;
           if constexpr (!Cfg::BIG) {
             if constexpr (PREFIX) {

@@ -486,7 +486,10 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     const long double w = weights ? (long double)weights[e] : (long double)k;
     wrow[w_off[k] + le] = (double)(w * Ckl[k]);
   }
+  // shared-prefix memo: per warp block (the NCW blocks of 32*epl consecutive sorted
+  // edges of a tile, one per consumer warp) the shared prefix length U
   std::vector<std::vector<uint8_t>> tile_u(N + 1);
+  const int nblk = p->ent.consumers / 32, wblk = tile / nblk;
   std::vector<int> wuni(N + 1, 0);
   std::vector<double> wconst(N + 1, 0.0);
   const bool memo = p->ent.prefix_mmax > 0 && !(flags & (STTSV_DETERMINISTIC | STTSV_NO_PREFIX_MEMO)) &&
@@ -549,17 +552,19 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     // shared-prefix memo (prefix.cuh): per tile, the number U of leading members
     // all its edges share = the common prefix of its first and last (sorted) edge
     const int64_t ntl = padded / tile;
-    tile_u[k].assign(ntl, 0);
+    tile_u[k].assign(ntl * nblk, 0);
     if (memo) {
       const int L = N - k + 1;
-      for (int64_t tl = 0; tl < ntl; ++tl) {
-        const int64_t j0 = tl * tile, j1 = j0 + tile - 1;
+      for (int64_t bl = 0; bl < ntl * nblk; ++bl) {  // warp blocks of wblk consecutive sorted edges
+        const int64_t j0 = bl * wblk, j1 = j0 + wblk - 1;
         int u = 0;
         while (u < k && col[(int64_t)u * st + j0] == col[(int64_t)u * st + j1]) ++u;
         const int M = k - u;
         const bool ok = u >= 1 && (M == 0 || (M <= p->ent.prefix_mmax && L <= p->ent.prefix_lmax));
-        tile_u[k][tl] = (uint8_t)(ok ? u : 0);
+        tile_u[k][bl] = (uint8_t)(ok ? u : 0);
       }
+    }
+  }
     }
   }
   std::vector<int32_t>().swap(rows);
@@ -608,25 +613,30 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     p->stored_inc += stored[k] * k;
     const int64_t ntl = (stored[k] + tile - 1) / tile;
     for (int64_t tl = 0; tl < ntl; ++tl) {
-      const int u = tile_u[k][tl];
-      const int64_t real = std::min<int64_t>(tile, stored[k] - tl * tile);  // edges of the tile that are not padding
-      p->stream_bytes += (int64_t)tile * (idb * (k - u) + (wuni[k] ? 0 : 8));
-      p->fma_exec += dp_fma_prefix(N, k, u) * (double)real;
-      if (u > 0) {
-        p->prefix_tiles += 1;
-        p->prefix_inc += (int64_t)u * real;
+      int us = k;  // staged columns: from the smallest prefix of the tile's blocks
+      for (int w = 0; w < nblk; ++w) us = std::min<int>(us, tile_u[k][tl * nblk + w]);
+      p->stream_bytes += (int64_t)tile * (idb * (k - us) + (wuni[k] ? 0 : 8));
+      for (int w = 0; w < nblk; ++w) {
+        const int u = tile_u[k][tl * nblk + w];
+        const int64_t first = tl * tile + (int64_t)w * wblk;
+        const int64_t real = std::max<int64_t>(0, std::min<int64_t>(wblk, stored[k] - first));  // not padding
+        p->fma_exec += dp_fma_prefix(N, k, u) * (double)real;
+        if (u > 0) {
+          p->prefix_tiles += 1;
+          p->prefix_inc += (int64_t)u * real;
+        }
       }
     }
   }
   kp.num_tiles = tiles;
   // shared-prefix groups: consecutive tiles (kernel order) with the same bucket, U and
   // prefix ids share a group id; U = 0 tiles have none (-1)
-  std::vector<long long> h_hdr;  // per tile (goff << 8) | U
+  std::vector<long long> h_hdr;  // per tile: U_stage; then per warp block (goff << 8) | U
   std::vector<int32_t> h_gku;
   std::vector<int64_t> h_goff;
   std::vector<double> h_gtab;  // group records (prefix.cuh): [A: L][C: U x L][ids: U]; ids filled here
   if (memo && p->prefix_tiles > 0) {
-    h_hdr.assign(tiles, 0);
+    h_hdr.assign((size_t)tiles * (1 + nblk), 0);
     int32_t gid = -1;
     int pk = -1, pu = -1;
     std::vector<int32_t> pref, cur;
@@ -636,26 +646,32 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       const int64_t ntl = (stored[k] + tile - 1) / tile;
       for (int64_t tl = 0; tl < ntl; ++tl) {
         const int64_t t = kp.b[i].tile_begin + tl;
-        const int u = tile_u[k][tl];
-        if (u == 0) {
-          pk = -1;
-          continue;
+        int us = k;
+        for (int w = 0; w < nblk; ++w) us = std::min<int>(us, tile_u[k][tl * nblk + w]);
+        h_hdr[(size_t)t * (1 + nblk)] = us;
+        for (int w = 0; w < nblk; ++w) {
+          const int u = tile_u[k][tl * nblk + w];
+          if (u == 0) {
+            pk = -1;
+            continue;
+          }
+          const int64_t j0 = tl * tile + (int64_t)w * wblk;
+          cur.assign(u, 0);
+          for (int q = 0; q < u; ++q) cur[q] = col[(int64_t)q * stride[k] + j0];
+          if (!(k == pk && u == pu && cur == pref)) {
+            ++gid;
+            pk = k;
+            pu = u;
+            pref = cur;
+            const int L = N - k + 1;
+            h_gku.push_back(k | (u << 8));
+            h_goff.push_back((int64_t)h_gtab.size());
+            h_gtab.resize(h_gtab.size() + L + (size_t)u * L + u, 0.0);
+            long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - u);
+            for (int q = 0; q < u; ++q) ids[q] = cur[q];
+          }
+          h_hdr[(size_t)t * (1 + nblk) + 1 + w] = ((long long)h_goff[gid] << 8) | u;
         }
-        cur.assign(u, 0);
-        for (int q = 0; q < u; ++q) cur[q] = col[(int64_t)q * stride[k] + tl * tile];
-        if (!(k == pk && u == pu && cur == pref)) {
-          ++gid;
-          pk = k;
-          pu = u;
-          pref = cur;
-          const int L = N - k + 1;
-          h_gku.push_back(k | (u << 8));
-          h_goff.push_back((int64_t)h_gtab.size());
-          h_gtab.resize(h_gtab.size() + L + (size_t)u * L + u, 0.0);
-          long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - u);
-          for (int q = 0; q < u; ++q) ids[q] = cur[q];
-        }
-        h_hdr[t] = ((long long)h_goff[gid] << 8) | u;
       }
     }
     p->prefix_groups = (int64_t)gid + 1;

@@ -28,7 +28,10 @@ for spec in sys.argv[2:]:
     vobjs = []
     for id16 in ([0, 1] if N in B.id16_ranks() else [0]):
         o = os.path.join(out, "edge%s_n%d_%s.o" % ("16" if id16 else "", N, name))
-        subprocess.check_call([B.NVCC] + B.NVFLAGS + flags + ["-DSTTSV_INST_N=%d" % N, "-DSTTSV_INST_ID16=%d" % id16,
+        # "16:-DFLAG" applies to the 16-bit-id object only (e.g. STTSV_WAITPROF: one
+        # object may define the debug counters)
+        fl = [f[3:] for f in flags if f.startswith("16:") and id16] + [f for f in flags if not f.startswith("16:")]
+        subprocess.check_call([B.NVCC] + B.NVFLAGS + fl + ["-DSTTSV_INST_N=%d" % N, "-DSTTSV_INST_ID16=%d" % id16,
                                "-c", os.path.join(B.CSRC, "edge_inst.cu"), "-o", o])
         vobjs.append(o)
     lib = os.path.join(out, "libsttsv_%s.so" % name)
