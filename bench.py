@@ -257,6 +257,19 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
 
+    def time_loop(fn):
+        for _ in range(args.warmup):
+            fn()
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        return max_over_ranks([b0.elapsed_time(b1) / args.steps])[0]
+
     for _ in range(args.warmup):
         plan.apply(x, y, stream)
     barrier()
@@ -286,6 +299,40 @@ def run_ours(args):
     plan.profile(False)
     kern_ms, kern_n = plan.profile_read()
     kern_avg = max_over_ranks([kern_ms / max(kern_n, 1)])[0]
+
+    # ---------------- A/B: the same product without the shared-prefix memo (every edge runs
+    # its full DP and streams all its ids and weight; the round-1 kernel structure)
+    nomemo = None
+    if not args.no_memo_report:
+        nplan = S.Plan.from_hypergraph(hg, device=dev_index, world=world, rank=rank, comm=comm,
+                                       flags=S.STTSV_NO_PREFIX_MEMO)
+        nms = time_loop(lambda: nplan.apply(x, y, stream))
+        nplan.profile(True)
+        for _ in range(args.steps):
+            nplan.apply(x, y, stream)
+        torch.cuda.synchronize(dev)
+        nplan.profile(False)
+        nk_ms, nk_n = nplan.profile_read()
+        nk = max_over_ranks([nk_ms / max(nk_n, 1)])[0]
+        ninfo = nplan.info()
+        peak_n, _ = measured_peaks()
+        fp64_n, _ = fp64_peak_tflops()
+        ns = ninfo["stream_bytes"] / (nk * 1e-3) / 1e9 / peak_n
+        nf = 2.0 * ninfo["fma_executed"] / (nk * 1e-3) / 1e12 / fp64_n
+        nomemo = {"value": hg.incidences / (nms * 1e-3), "unit": UNIT, "ms_per_step": nms, "kernel_ms": nk,
+                  "stream_bytes": ninfo["stream_bytes"], "fma": ninfo["fma_executed"],
+                  "binding_frac": max(ns, nf), "hbm_stream_frac": ns, "fp64_frac": nf,
+                  "note": "STTSV_NO_PREFIX_MEMO plan: the per-edge kernel without the shared-prefix memo (A/B)"}
+        nplan.close()
+        del nplan
+    memo = {"enabled": info["prefix_tiles"] > 0, "prefix_blocks": info["prefix_tiles"],
+            "blocks": info["num_tiles"] * (info["kernel_block"] // 32 - 1), "tiles": info["num_tiles"],
+            "groups": info["prefix_groups"], "prefix_incidences": info["prefix_incidences"],
+            "fma_executed": info["fma_executed"], "fma_appA": info["fma_per_apply"],
+            "stream_bytes": info["stream_bytes"],
+            "note": "shared-prefix memo (SURVEY.md f3, DESIGN.md §4): warp blocks whose edges share a sorted member "
+                    "prefix run the DP over their own members; the prefix members' totals come from a per-apply "
+                    "group table"}
 
     shard_check = None
     if world > 1 and args.no_comm:
@@ -331,7 +378,7 @@ def run_ours(args):
     fp64_peak, fp64_src = fp64_peak_tflops()
     ksec = kern_avg * 1e-3
     stream_gbs = phys_bytes / ksec / 1e9
-    fp64_tf = 2.0 * info["fma_per_apply"] / ksec / 1e12
+    fp64_tf = 2.0 * info["fma_executed"] / ksec / 1e12     # FP64 operations the kernel executes
     stream_frac, fp64_frac = stream_gbs / peak, fp64_tf / fp64_peak
     traffic = ncu_traffic(args.config)
     if stream_frac >= fp64_frac:
@@ -350,7 +397,11 @@ def run_ours(args):
                    "note": "bytes the kernel streams (member ids as uint16 when n_active <= 65536) + x_a/y_a; "
                            "compare with traffic (ncu DRAM bytes per launch)"},
         "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_frac, "peak_source": fp64_src,
-                 "flops_def": "2 x (FMAs of the per-edge DP, SURVEY.md App. A, + k+1 scalings) per edge"},
+                 "flops_def": "2 x the FP64 operations the kernel executes (plan_info fma_executed: the per-edge DP "
+                              "over each edge's own members after the shared-prefix memo, DESIGN.md §4)",
+                 "appA_tflops": 2.0 * info["fma_per_apply"] / ksec / 1e12,
+                 "appA_def": "secondary: 2 x (SURVEY.md App. A FMAs + k+1 scalings) per input edge, i.e. the work of "
+                             "the per-edge DP without the memo"},
         "hbm_alg": {"bytes_per_launch": alg_bytes, "gbs": alg_bytes / ksec / 1e9, "frac": alg_bytes / ksec / 1e9 / peak,
                     "def": "secondary: SURVEY.md 8(d) algorithmic bytes of the int32/fp64 store: 4*sum|e| + 8*m "
                            "+ 16*n_active per shard"}})
@@ -359,19 +410,6 @@ def run_ours(args):
     # (identical vertex sets merged at plan time, weights summed; B is linear in
     # w).  Reported beside the headline, never as it: the headline stores and
     # processes every input hyperedge.
-    def time_loop(fn):
-        for _ in range(args.warmup):
-            fn()
-        barrier()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0.record(stream)
-        for _ in range(args.steps):
-            fn()
-        b1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        return max_over_ranks([b0.elapsed_time(b1) / args.steps])[0]
-
     merged = None
     if not args.no_merge_report:
         mplan = S.Plan.from_hypergraph(hg, device=dev_index, world=world, rank=rank, comm=comm,
@@ -420,7 +458,8 @@ def run_ours(args):
                                                                     if world > 1 else "none")},
                "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
                / (ms_step * 1e-3) / 1e9,
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "merge_duplicates": merged, "batch": batch,
+               "roofline": roofline, "memo": memo, "no_memo": nomemo, "cpu_baseline": cpu, "e2e": e2e,
+               "merge_duplicates": merged, "batch": batch,
                "gpu_launches": plan.launches() * args.steps, "clocks": sampler.summary()}
         if shard_check is not None:
             out["shard_check"] = shard_check
@@ -444,6 +483,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merge-report", action="store_true")
     ap.add_argument("--no-batch-report", action="store_true")
+    ap.add_argument("--no-memo-report", action="store_true")
     ap.add_argument("--no-comm", action="store_true",
                     help="N>1 harness without the NCCL data plane (ranks may share a GPU; host-side shard sum)")
     args = ap.parse_args()

@@ -36,9 +36,13 @@ def id16_ranks() -> list[int]:
     return [int(v) for v in re.findall(r"X\((\d+)\)", m.group(1))]
 
 
-def _newest_dep() -> float:
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "sttsv.h")]
+def _newest(*names) -> float:
+    deps = [os.path.join(CSRC, f) for f in names] + [os.path.join(ROOT, "include", "sttsv.h"),
+                                                   os.path.join(CSRC, "internal.h")]
     return max(os.path.getmtime(d) for d in deps)
+
+
+_DEVICE_HDRS = ("edge_kernel.cuh", "dp.cuh", "prefix.cuh")
 
 
 def _run(cmd):
@@ -50,27 +54,30 @@ def _run(cmd):
 
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    newest = _newest_dep()
+    t_edge = _newest("edge_inst.cu", *_DEVICE_HDRS)
+    t_kern = _newest("kernels.cu", *_DEVICE_HDRS)
+    t_plan = _newest("plan.cpp")
     jobs = jobs or max(1, os.cpu_count() or 1)
     units = []
     for n in compiled_ranks() + [0]:
-        units.append((os.path.join(OBJ, "edge_n%d.o" % n),
+        units.append((os.path.join(OBJ, "edge_n%d.o" % n), t_edge,
                       [NVCC] + NVFLAGS + ["-DSTTSV_INST_N=%d" % n, "-c", os.path.join(CSRC, "edge_inst.cu")]))
     for n in id16_ranks():
-        units.append((os.path.join(OBJ, "edge16_n%d.o" % n),
+        units.append((os.path.join(OBJ, "edge16_n%d.o" % n), t_edge,
                       [NVCC] + NVFLAGS + ["-DSTTSV_INST_N=%d" % n, "-DSTTSV_INST_ID16=1", "-c",
                                           os.path.join(CSRC, "edge_inst.cu")]))
-    units.append((os.path.join(OBJ, "kernels.o"), [NVCC] + NVFLAGS + ["-c", os.path.join(CSRC, "kernels.cu")]))
-    units.append((os.path.join(OBJ, "plan.o"),
+    units.append((os.path.join(OBJ, "kernels.o"), t_kern,
+                  [NVCC] + NVFLAGS + ["-c", os.path.join(CSRC, "kernels.cu")]))
+    units.append((os.path.join(OBJ, "plan.o"), t_plan,
                   [NVCC] + NVFLAGS + ["-Xcompiler", "-fopenmp", "-c", os.path.join(CSRC, "plan.cpp")]))
-    todo = [(o, c + ["-o", o]) for o, c in units
-            if force or not os.path.exists(o) or os.path.getmtime(o) < newest]
+    todo = [(o, c + ["-o", o]) for o, t, c in units
+            if force or not os.path.exists(o) or os.path.getmtime(o) < t]
     if todo:
         with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
             for out in ex.map(lambda oc: _run(oc[1]), todo):
                 if verbose and out.strip():
                     print(out, file=sys.stderr)
-    objs = [o for o, _ in units]
+    objs = [o for o, _, _ in units]
     if force or todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl", "-lgomp"])
     return LIB

@@ -565,8 +565,6 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       }
     }
   }
-    }
-  }
   std::vector<int32_t>().swap(rows);
   std::vector<double>().swap(wrow);
   std::vector<int32_t>().swap(newid);

@@ -33,7 +33,7 @@ def test_bench_torchrun_world2_no_comm():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "5", "--warmup", "3", "--config", "mid", "--no-comm",
-           "--no-merge-report", "--no-batch-report", "--cpu-seconds", "1"]
+           "--no-merge-report", "--no-batch-report", "--no-memo-report", "--cpu-seconds", "1"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     d = _last_json(r.stdout)
@@ -49,7 +49,7 @@ def test_bench_single_gpu_contract():
     """One short N=1 run of the default workload path on a small config: the keys the
     driver reads are present and consistent."""
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "5", "--warmup", "3", "--config", "mid",
-           "--no-merge-report", "--no-batch-report", "--cpu-seconds", "1"]
+           "--no-merge-report", "--no-batch-report", "--no-memo-report", "--cpu-seconds", "1"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     d = _last_json(r.stdout)
