@@ -76,7 +76,7 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 #define STTSV_EPL16 8
 #endif
 #ifndef STTSV_RING_KB
-#define STTSV_RING_KB 112
+#define STTSV_RING_KB 108
 #endif
 #ifndef STTSV_NCW_SMALL
 #define STTSV_NCW_SMALL 7
