@@ -54,54 +54,80 @@ __global__ void series_kernel(const double* __restrict__ xa, double* __restrict_
     series_row(xa[i], xg + i * gs, gs, norm);
 }
 
-// Shared-prefix group table (prefix.cuh), one warp per group: lane i < U forms,
-// from the normalised series rows of the group's U prefix members, A_{\i} and
-// A = prod g_j in the same pass and writes C_i[j] = A_{\i}[D-j] + A[D-1-j]
-// (unnormalised coefficients; the second term for j <= D-1); lane 0 also writes
-// the front A (row format).  The edge kernel that follows is a programmatic
-// dependent launch (its consumers wait for this grid before reading the table).
-__global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
-                             const int64_t* __restrict__ goff, const double* gtab_in, double* gtab,
-                             int64_t ngroups) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < ngroups; g += warps) {
-    const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1, D = L - 1;
-    double* T = gtab + goff[g];
-    const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
-    if (gtab_in != gtab)  // a batch vector's copy of the table: carry the prefix ids over
-      for (int i = lane; i < U; i += 32) reinterpret_cast<long long*>(T + L + U * L)[i] = ids[i];
-    for (int i = lane; i < U; i += 32) {
-      double ah[STTSV_MAX_RANK], ai[STTSV_MAX_RANK];
-      double X = 1.0, Xi = 1.0;
-      ah[0] = ai[0] = 1.0;
-      for (int j = 1; j < L; ++j) ah[j] = ai[j] = 0.0;
-      for (int m = 0; m < U; ++m) {
-        const double* h = xg + (size_t)ids[m] * gs;
-        const bool in = m != i;
-        for (int j = L - 1; j >= 1; --j) {  // truncated products with implicit leading 1 (descending: in place)
-          const double hj = __ldg(h + j);
-          double s = ah[j] + hj, si = ai[j] + hj;
-          for (int q = 1; q < j; ++q) {
-            const double hq = __ldg(h + j - q);
-            s = fma(ah[q], hq, s);
-            si = fma(ai[q], hq, si);
-          }
-          ah[j] = s;
-          if (in) ai[j] = si;
-        }
-        const double x = __ldg(h);
-        X *= x;
-        if (in) Xi *= x;
+// Shared-prefix group table (prefix.cuh), one thread per (group, prefix member i):
+// from the normalised series rows of the group's U prefix members it forms, in
+// one pass over the rows, A_{\i} and A = prod g_j (compile-time L: register
+// arrays) and writes C_i[j] = A_{\i}[D-j] + A[D-1-j] (unnormalised coefficients;
+// the second term for j <= D-1); the i = 0 thread also writes the front A (row
+// format) and, for a batch vector's copy of the table, the prefix ids.  The edge
+// kernel that follows is a programmatic dependent launch (its consumers wait for
+// this grid before reading the table).
+template <int L>
+__device__ __forceinline__ void group_item(const double* __restrict__ xg, int gs, const long long* ids, int U, int i,
+                                           double* T, long long* ids_out) {
+  constexpr int D = L - 1;
+  double ah[L], ai[L];
+  double X = 1.0, Xi = 1.0;
+  ah[0] = ai[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j < L; ++j) ah[j] = ai[j] = 0.0;
+#pragma unroll 1
+  for (int m = 0; m < U; ++m) {
+    double h[L];
+    load_series<L>(xg + (size_t)ids[m] * gs, h);
+    const bool in = m != i;
+#pragma unroll
+    for (int j = L - 1; j >= 1; --j) {  // truncated products with implicit leading 1 (descending: in place)
+      double s = ah[j] + h[j], si = ai[j] + h[j];
+#pragma unroll
+      for (int q = 1; q < j; ++q) {
+        s = fma(ah[q], h[j - q], s);
+        si = fma(ai[q], h[j - q], si);
       }
-      if (i == 0) {
-        T[0] = X;
-        for (int j = 1; j < L; ++j) T[j] = ah[j];
-      }
-      double* C = T + L + i * L;
-      for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
+      ah[j] = s;
+      ai[j] = in ? si : ai[j];
     }
+    X *= h[0];
+    Xi = in ? Xi * h[0] : Xi;
+  }
+  if (i == 0) {
+    T[0] = X;
+#pragma unroll
+    for (int j = 1; j < L; ++j) T[j] = ah[j];
+    if (ids_out)
+      for (int m = 0; m < U; ++m) ids_out[m] = ids[m];
+  }
+  double* C = T + L + i * L;
+#pragma unroll
+  for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
+}
+
+template <int L>
+__device__ __forceinline__ void group_item_dispatch(int L_rt, const double* xg, int gs, const long long* ids, int U,
+                                                    int i, double* T, long long* ids_out) {
+  if constexpr (L <= STTSV_MAX_RANK) {
+    if (L_rt == L) {
+      group_item<L>(xg, gs, ids, U, i, T, ids_out);
+      return;
+    }
+    group_item_dispatch<L + 1>(L_rt, xg, gs, ids, U, i, T, ids_out);
+  }
+}
+
+__global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
+                             const int64_t* __restrict__ goff, const long long* __restrict__ items,
+                             int64_t nitems, const double* gtab_in, double* gtab) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nitems;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const long long it = items[t];
+    const int64_t g = it >> 8;
+    const int i = (int)(it & 255);
+    const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1;
+    const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
+    double* T = gtab + goff[g];
+    long long* ids_out = gtab_in != gtab ? reinterpret_cast<long long*>(T + L + U * L) : nullptr;
+    group_item_dispatch<1>(L, xg, gs, ids, U, i, T, ids_out);
   }
 }
 
@@ -367,9 +393,10 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 }
 
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
-                          const double* gtab_in, double* gtab_out, int64_t ngroups, cudaStream_t s) {
-  if (ngroups <= 0) return cudaSuccess;
-  group_kernel<<<grid_for(ngroups * 32, 128, 4096), 128, 0, s>>>(xg, gs, N, gku, goff, gtab_in, gtab_out, ngroups);
+                          const long long* items, int64_t nitems, const double* gtab_in, double* gtab_out,
+                          cudaStream_t s) {
+  if (nitems <= 0) return cudaSuccess;
+  group_kernel<<<grid_for(nitems, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
   return cudaGetLastError();
 }
 
