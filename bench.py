@@ -373,7 +373,9 @@ def run_ours(args):
     # binding roof = the larger of (bytes the kernel actually streams / HBM peak) and
     # (FP64 flops / FP64 peak); the SURVEY.md 8(d) int32-id byte count is secondary
     alg_bytes = 4 * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
-    phys_bytes = info["id_bytes"] * info["incidences"] + 8 * info["num_edges"] + 16 * info["n_active"]
+    # bytes the kernel streams: the plan's edge stream (ids of the columns not shared by a
+    # warp block's prefix, weights unless uniform) + x_a/y_a
+    phys_bytes = info["stream_bytes"] + 16 * info["n_active"]
     peak, peak_src = measured_peaks()
     fp64_peak, fp64_src = fp64_peak_tflops()
     ksec = kern_avg * 1e-3
@@ -394,8 +396,9 @@ def run_ours(args):
                             "FP64 DFMA pipe"},
         "stream": {"id_bytes": info["id_bytes"], "bytes_per_launch": phys_bytes, "gbs": stream_gbs,
                    "frac": stream_frac, "peak_source": peak_src,
-                   "note": "bytes the kernel streams (member ids as uint16 when n_active <= 65536) + x_a/y_a; "
-                           "compare with traffic (ncu DRAM bytes per launch)"},
+                   "note": "bytes the kernel streams: plan_info stream_bytes (uint16 ids when n_active <= 65536; no "
+                           "shared-prefix columns; no weights for uniform-weight buckets) + x_a/y_a; compare with "
+                           "traffic (ncu DRAM bytes per launch)"},
         "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "frac": fp64_frac, "peak_source": fp64_src,
                  "flops_def": "2 x the FP64 operations the kernel executes (plan_info fma_executed: the per-edge DP "
                               "over each edge's own members after the shared-prefix memo, DESIGN.md §4)",

@@ -1127,6 +1127,18 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
     constexpr bool PREFIX = Cfg::PMAX > 0 && !Cfg::BIG && !DET;
     double* const sred = sred_all + warp * Cfg::SCR_DOUBLES;
     bool any = false;
+    // programmatic dependent launch: x_a, the series table and y_a are written
+    // by the prologue grid (no-op when launched without the PDL attribute).  Behind
+    // the group kernel (p.group_wait) only the group table comes from the preceding
+    // grid: the wait is deferred to the first read of the table (gready).
+    bool gready = !p.group_wait;
+    if (gready) griddep_wait();
+    auto need_groups = [&]() {
+      if (!gready) {
+        griddep_wait();
+        gready = true;
+      }
+    };
     // pending M = 0 prefix group (prefix.cuh): consecutive tiles whose edges are all one
     // vertex set of the same group only add their weights (this lane's share) here;
     // the group's totals are deposited once, when another M = 0 group starts or at the end
@@ -1134,6 +1146,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
     int pend_L = 0, pend_U = 0;
     double pend_w = 0.0;
     auto flush_pending = [&]() {
+      need_groups();
       double t0 = pend_w;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t0 += __shfl_xor_sync(kFull, t0, o);
@@ -1141,9 +1154,6 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         prefix_tile_flush0(t0, p.gtab + (size_t)v * p.gtab_vstride + pend_goff, pend_L, pend_U,
                            Sink{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H}, lane);
     };
-    // programmatic dependent launch: x_a, the series table and y_a are written
-    // by the prologue grid (no-op when launched without the PDL attribute)
-    griddep_wait();
 #if STTSV_WAITPROF
     long long wait_cyc = 0;
     const long long c_start = clock64();
@@ -1221,6 +1231,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
           if constexpr (!Cfg::BIG) {
             if constexpr (PREFIX) {
               if (tu > 0) {
+                need_groups();
                 dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT>(k, tu, sids, sw, base, xgv, Gv, ra, skv, sred,
                                                                    lane);
                 done = true;
@@ -1231,6 +1242,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
             const int col = warp * 32 + lane;  // EPL = 1
             if constexpr (Cfg::BIG_PREFIX && !DET) {
               if (tu > 0) {  // shared-prefix tile (prefix.cuh); warp-uniform
+                need_groups();
 #if STTSV_BIG_LOCAL
                 dispatch_big_prefix<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col), sw,
                                                             warp * 32, Gv, xgv, p.gs, lstk, ra, skv, sred, lane);

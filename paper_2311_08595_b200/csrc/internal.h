@@ -63,6 +63,8 @@ struct EdgeKernelParams {
   const long long* tile_hdr;
   const double* gtab;    // per-apply group table (prefix.cuh)
   int64_t gtab_vstride;  // doubles between the group tables of consecutive vectors (batch)
+  int32_t group_wait;    // 1: the preceding grid is group_kernel (consumers wait for it only before their
+                         // first group-table read; x_a / the series table come from an earlier, completed grid)
 };
 
 // Ranks with a fully unrolled edge kernel (one object file each); every other

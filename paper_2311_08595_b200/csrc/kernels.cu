@@ -71,24 +71,33 @@ __device__ __forceinline__ void group_item(const double* __restrict__ xg, int gs
   ah[0] = ai[0] = 1.0;
 #pragma unroll
   for (int j = 1; j < L; ++j) ah[j] = ai[j] = 0.0;
+  // rows in batches of B (their loads issued together)
+  constexpr int B = L <= 6 ? 4 : (L <= 12 ? 2 : 1);
 #pragma unroll 1
-  for (int m = 0; m < U; ++m) {
-    double h[L];
-    load_series<L>(xg + (size_t)ids[m] * gs, h);
-    const bool in = m != i;
+  for (int m0 = 0; m0 < U; m0 += B) {
+    double hb[B][L];
 #pragma unroll
-    for (int j = L - 1; j >= 1; --j) {  // truncated products with implicit leading 1 (descending: in place)
-      double s = ah[j] + h[j], si = ai[j] + h[j];
+    for (int b = 0; b < B; ++b)
+      if (m0 + b < U) load_series<L>(xg + (size_t)ids[m0 + b] * gs, hb[b]);
 #pragma unroll
-      for (int q = 1; q < j; ++q) {
-        s = fma(ah[q], h[j - q], s);
-        si = fma(ai[q], h[j - q], si);
+    for (int b = 0; b < B; ++b) {
+      if (m0 + b >= U) break;
+      const double(&h)[L] = hb[b];
+      const bool in = m0 + b != i;
+#pragma unroll
+      for (int j = L - 1; j >= 1; --j) {  // truncated products with implicit leading 1 (descending: in place)
+        double s = ah[j] + h[j], si = ai[j] + h[j];
+#pragma unroll
+        for (int q = 1; q < j; ++q) {
+          s = fma(ah[q], h[j - q], s);
+          si = fma(ai[q], h[j - q], si);
+        }
+        ah[j] = s;
+        ai[j] = in ? si : ai[j];
       }
-      ah[j] = s;
-      ai[j] = in ? si : ai[j];
+      X *= h[0];
+      Xi = in ? Xi * h[0] : Xi;
     }
-    X *= h[0];
-    Xi = in ? Xi * h[0] : Xi;
   }
   if (i == 0) {
     T[0] = X;

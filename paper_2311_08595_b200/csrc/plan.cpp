@@ -841,6 +841,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.tile_hdr = h_hdr.empty() ? nullptr : d_hdr;
   kp.gtab = h_gtab.empty() ? nullptr : d_gtab;
   kp.gtab_vstride = 0;
+  kp.group_wait = kp.gtab != nullptr;  // every launch of a plan with groups follows the group kernel
   p->gtab_doubles = (int64_t)h_gtab.size();
   p->d_gku = d_gku;
   p->d_goff = d_goff;
@@ -1237,6 +1238,7 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
         kp.gtab = p->b_gtab;
         kp.gtab_vstride = p->gtab_doubles;
       }
+      kp.group_wait = groups;
       CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0), groups),
                "edge kernel launch");
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,
