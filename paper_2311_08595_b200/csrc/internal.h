@@ -128,10 +128,12 @@ cudaError_t launch_prologue(const double* x, const int32_t* act, double* xa, dou
 cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_t n_active, cudaStream_t s);
 // shared-prefix group table (prefix.cuh): A and the rows C_i of every group from
 // the series table; gku[g] = k | U << 8
-// gtab_in: the plan's table (its prefix ids); gtab_out receives A, C (and the ids
-// when it is a batch vector's copy)
+// items[t] = (group << 8) | i, one per prefix member of every group; gtab_in: the
+// plan's table (its prefix ids); gtab_out receives A, C (and the ids when it is a
+// batch vector's copy)
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
-                          int64_t ngroups, const double* gtab_in, double* gtab_out, cudaStream_t s);
+                          const long long* items, int64_t nitems, const double* gtab_in, double* gtab_out,
+                          cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)
 cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, int norm, double* partial,

@@ -54,61 +54,80 @@ __global__ void series_kernel(const double* __restrict__ xa, double* __restrict_
     series_row(xa[i], xg + i * gs, gs, norm);
 }
 
-// Shared-prefix group table (prefix.cuh), one warp per group, lane j holding
-// coefficient j of a normalised series (lane 0: the scalar x-product, lanes
-// 1..L-1: the coefficients under the implicit leading 1).  From the group's U
-// prefix rows it forms the prefix products P_m = g_0..g_m and suffix products
-// S_m = g_m..g_{U-1}, then A = P_{U-1}, A_{\i} = P_{i-1} S_{i+1}, and writes the
-// front A (row format) and C_i[j] = A_{\i}[D-j] + A[D-1-j] (unnormalised; the
-// second term for j <= D-1).  The edge kernel that follows is a programmatic
-// dependent launch (its consumers wait for this grid before the first table read).
-__device__ __forceinline__ double gmul(double a, double h, int lane, int L) {
-  // (a*h) mod t^L of two lane-distributed normalised series; lane 0: scalar product
-  double s = lane == 0 ? a * h : a + h;
-  for (int q = 1; q < L - 1; ++q) {
-    const double aq = __shfl_sync(0xffffffffu, a, q);
-    const double hq = __shfl_sync(0xffffffffu, h, (lane - q) & 31);
-    if (lane > q && lane < L) s = fma(aq, hq, s);
+// Shared-prefix group table (prefix.cuh), one thread per (group, prefix member i):
+// from the normalised series rows of the group's U prefix members it forms, in
+// one pass over the rows, A_{\i} and A = prod g_j (compile-time L: register
+// arrays) and writes C_i[j] = A_{\i}[D-j] + A[D-1-j] (unnormalised coefficients;
+// the second term for j <= D-1); the i = 0 thread also writes the front A (row
+// format) and, for a batch vector's copy of the table, the prefix ids.  The edge
+// kernel that follows is a programmatic dependent launch (its consumers wait for
+// this grid before reading the table).
+template <int L>
+__device__ __forceinline__ void group_item(const double* __restrict__ xg, int gs, const long long* ids, int U, int i,
+                                           double* T, long long* ids_out) {
+  constexpr int D = L - 1;
+  double ah[L], ai[L];
+  double X = 1.0, Xi = 1.0;
+  ah[0] = ai[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j < L; ++j) ah[j] = ai[j] = 0.0;
+#pragma unroll 1
+  for (int m = 0; m < U; ++m) {
+    double h[L];
+    load_series<L>(xg + (size_t)ids[m] * gs, h);
+    const bool in = m != i;
+#pragma unroll
+    for (int j = L - 1; j >= 1; --j) {  // truncated products with implicit leading 1 (descending: in place)
+      double s = ah[j] + h[j], si = ai[j] + h[j];
+#pragma unroll
+      for (int q = 1; q < j; ++q) {
+        s = fma(ah[q], h[j - q], s);
+        si = fma(ai[q], h[j - q], si);
+      }
+      ah[j] = s;
+      ai[j] = in ? si : ai[j];
+    }
+    X *= h[0];
+    Xi = in ? Xi * h[0] : Xi;
   }
-  return lane < L ? s : 0.0;
+  if (i == 0) {
+    T[0] = X;
+#pragma unroll
+    for (int j = 1; j < L; ++j) T[j] = ah[j];
+    if (ids_out)
+      for (int m = 0; m < U; ++m) ids_out[m] = ids[m];
+  }
+  double* C = T + L + i * L;
+#pragma unroll
+  for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
+}
+
+template <int L>
+__device__ __forceinline__ void group_item_dispatch(int L_rt, const double* xg, int gs, const long long* ids, int U,
+                                                    int i, double* T, long long* ids_out) {
+  if constexpr (L <= STTSV_MAX_RANK) {
+    if (L_rt == L) {
+      group_item<L>(xg, gs, ids, U, i, T, ids_out);
+      return;
+    }
+    group_item_dispatch<L + 1>(L_rt, xg, gs, ids, U, i, T, ids_out);
+  }
 }
 
 __global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
-                             const int64_t* __restrict__ goff, int64_t ngroups, const double* gtab_in,
-                             double* gtab) {
+                             const int64_t* __restrict__ goff, const long long* __restrict__ items,
+                             int64_t nitems, const double* gtab_in, double* gtab) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < ngroups; g += warps) {
-    const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1, D = L - 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nitems;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const long long it = items[t];
+    const int64_t g = it >> 8;
+    const int i = (int)(it & 255);
+    const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1;
     const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
     double* T = gtab + goff[g];
-    double hr[STTSV_MAX_RANK], P[STTSV_MAX_RANK], Sf[STTSV_MAX_RANK];  // per-lane values (local memory)
-    for (int m = 0; m < U; ++m) hr[m] = (lane < L && lane < gs) ? __ldg(xg + (size_t)ids[m] * gs + lane) : 0.0;
-    double acc = hr[0];
-    P[0] = acc;
-    for (int m = 1; m < U; ++m) P[m] = acc = gmul(acc, hr[m], lane, L);
-    acc = hr[U - 1];
-    Sf[U - 1] = acc;
-    for (int m = U - 2; m >= 0; --m) Sf[m] = acc = gmul(hr[m], acc, lane, L);
-    const double A = P[U - 1];
-    const double one = lane == 0 ? 1.0 : 0.0;  // the empty product
-    if (lane < L) T[lane] = A;
-    const double Xa = __shfl_sync(0xffffffffu, A, 0);
-    for (int i = 0; i < U; ++i) {
-      const double lo = i > 0 ? P[i - 1] : one, hi = i + 1 < U ? Sf[i + 1] : one;
-      const double Ai = gmul(lo, hi, lane, L);
-      const double Xi = __shfl_sync(0xffffffffu, Ai, 0);
-      // lane j: C_i[j] = X_i ah_i[D-j] + X_A ah[D-1-j]  (ah[0] = 1)
-      const double ai = __shfl_sync(0xffffffffu, Ai, (D - lane) & 31);
-      const double aa = __shfl_sync(0xffffffffu, A, (D - 1 - lane) & 31);
-      if (lane <= D) {
-        const double t1 = Xi * (lane == D ? 1.0 : ai);
-        const double t2 = lane <= D - 1 ? Xa * (lane == D - 1 ? 1.0 : aa) : 0.0;
-        T[L + i * L + lane] = t1 + t2;
-      }
-    }
-    if (gtab_in != gtab && lane < U) reinterpret_cast<long long*>(T + L + U * L)[lane] = ids[lane];
+    long long* ids_out = gtab_in != gtab ? reinterpret_cast<long long*>(T + L + U * L) : nullptr;
+    group_item_dispatch<1>(L, xg, gs, ids, U, i, T, ids_out);
   }
 }
 
@@ -374,9 +393,10 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 }
 
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
-                          int64_t ngroups, const double* gtab_in, double* gtab_out, cudaStream_t s) {
-  if (ngroups <= 0) return cudaSuccess;
-  group_kernel<<<grid_for(ngroups * 32, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, ngroups, gtab_in, gtab_out);
+                          const long long* items, int64_t nitems, const double* gtab_in, double* gtab_out,
+                          cudaStream_t s) {
+  if (nitems <= 0) return cudaSuccess;
+  group_kernel<<<grid_for(nitems, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
   return cudaGetLastError();
 }
 

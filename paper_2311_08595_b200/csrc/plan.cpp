@@ -269,6 +269,8 @@ struct sttsv_plan_s {
   double fma_exec = 0;      // FP64 operations the kernel executes per apply (shared-prefix memo counted)
   const int32_t* d_gku = nullptr;  // per prefix group: k | U << 8 (group_kernel)
   const int64_t* d_goff = nullptr;  // per prefix group: offset of its record in the group table
+  const long long* d_items = nullptr;  // group_kernel work items
+  int64_t nitems = 0;
   int64_t prefix_tiles = 0, prefix_groups = 0, prefix_inc = 0;
   // edge-kernel timing (sttsv_plan_profile)
   bool profiling = false;
@@ -589,7 +591,16 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<int> order;
   for (int k = 1; k <= N; ++k)
     if (mk[k] > 0) order.push_back(k);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dp_fma(N, a) > dp_fma(N, b); });
+  // per-edge cost of a bucket as the kernel will execute it (the shared-prefix memo
+  // makes most of a bucket cheap; its unshared blocks cost the full DP)
+  std::vector<double> ecost(N + 1, 0.0);
+  for (int k = 1; k <= N; ++k) {
+    if (mk[k] == 0) continue;
+    double c = 0;
+    for (size_t bl = 0; bl < tile_u[k].size(); ++bl) c += dp_fma_prefix(N, k, tile_u[k][bl]);
+    ecost[k] = tile_u[k].empty() ? dp_fma(N, k) : c / (double)tile_u[k].size();
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ecost[a] > ecost[b]; });
   EdgeKernelParams& kp = p->kp;
   kp.N = N;
   kp.nb = (int)order.size();
@@ -634,6 +645,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<int32_t> h_gku;
   std::vector<int64_t> h_goff;
   std::vector<double> h_gtab;  // group records (prefix.cuh): [A: L][C: U x L][ids: U]; ids filled here
+  std::vector<long long> h_items;  // group_kernel work items: (group << 8) | prefix member
   std::map<std::vector<int32_t>, int32_t> gmap;
   if (memo && p->prefix_tiles > 0) {
     h_hdr.assign((size_t)tiles * (1 + nblk), 0);
@@ -678,6 +690,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
               h_gtab.resize(h_gtab.size() + L + (size_t)u * L + u, 0.0);
               long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - u);
               for (int q = 0; q < u; ++q) ids[q] = cur[q];
+              for (int q = 0; q < u; ++q) h_items.push_back(((long long)gid << 8) | q);
             }
           }
           h_hdr[(size_t)t * (1 + nblk) + 1 + w] = ((long long)h_goff[gid] << 8) | u;
@@ -796,8 +809,9 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   const size_t b_priv = align((size_t)grid * H * 8 + 8);
   const size_t b_tu = align(h_hdr.size() * 8 + 8), b_tg = 0;
   const size_t b_gku = align(h_gku.size() * 4 + 4), b_goff = align(h_goff.size() * 8 + 8),
-               b_gtab = align(h_gtab.size() * 8 + 8);
-  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg + b_gku + b_goff + b_gtab;
+               b_gtab = align(h_gtab.size() * 8 + 8), b_items = align(h_items.size() * 8 + 8);
+  p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg + b_gku + b_goff + b_gtab +
+              b_items;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -815,6 +829,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   int32_t* d_gku = (int32_t*)gbase;
   int64_t* d_goff = (int64_t*)(gbase + b_gku);
   double* d_gtab = (double*)(gbase + b_gku + b_goff);
+  long long* d_items = (long long*)(gbase + b_gku + b_goff + b_gtab);
   p->gs = gs;
   if (ids_total && idb == 4) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ids_total && idb == 2) {
@@ -828,6 +843,10 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (ce == cudaSuccess && !h_gku.empty()) ce = cudaMemcpy(d_gku, h_gku.data(), h_gku.size() * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_goff.empty()) ce = cudaMemcpy(d_goff, h_goff.data(), h_goff.size() * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_gtab.empty()) ce = cudaMemcpy(d_gtab, h_gtab.data(), h_gtab.size() * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_items.empty())
+    ce = cudaMemcpy(d_items, h_items.data(), h_items.size() * 8, cudaMemcpyHostToDevice);
+  p->d_items = d_items;
+  p->nitems = (int64_t)h_items.size();
   kp.tile_hdr = h_hdr.empty() ? nullptr : d_hdr;
   kp.gtab = h_gtab.empty() ? nullptr : d_gtab;
   kp.gtab_vstride = 0;
@@ -972,7 +991,7 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
     }
     const bool groups = p->kp.gtab != nullptr;
     if (groups)  // per-apply shared-prefix group table (prefix.cuh)
-      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->prefix_groups, p->kp.gtab,
+      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->d_items, p->nitems, p->kp.gtab,
                              const_cast<double*>(p->kp.gtab), s), "group kernel launch");
     CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed || groups),
              "edge kernel launch");
@@ -1222,8 +1241,8 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       const bool groups = p->kp.gtab != nullptr;
       if (groups) {
         for (int v = 0; v < nvec; ++v)
-          CUDA_TRY(launch_groups(p->b_xg + (size_t)v * na * p->gs, p->gs, p->N, p->d_gku, p->d_goff,
-                                 p->prefix_groups, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles, s),
+          CUDA_TRY(launch_groups(p->b_xg + (size_t)v * na * p->gs, p->gs, p->N, p->d_gku, p->d_goff, p->d_items,
+                                 p->nitems, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles, s),
                    "group kernel launch");
         kp.gtab = p->b_gtab;
         kp.gtab_vstride = p->gtab_doubles;
