@@ -102,21 +102,25 @@ __device__ __forceinline__ void group_item(const double* __restrict__ xg, int gs
   for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
 }
 
-template <int L>
+template <int L, int LMAX>
 __device__ __forceinline__ void group_item_dispatch(int L_rt, const double* xg, int gs, const long long* ids, int U,
                                                     int i, double* T, long long* ids_out) {
-  if constexpr (L <= STTSV_MAX_RANK) {
+  if constexpr (L <= LMAX) {
     if (L_rt == L) {
       group_item<L>(xg, gs, ids, U, i, T, ids_out);
       return;
     }
-    group_item_dispatch<L + 1>(L_rt, xg, gs, ids, U, i, T, ids_out);
+    group_item_dispatch<L + 1, LMAX>(L_rt, xg, gs, ids, U, i, T, ids_out);
   }
 }
 
-__global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const int32_t* __restrict__ gku,
-                             const int64_t* __restrict__ goff, const long long* __restrict__ items,
-                             int64_t nitems, const double* gtab_in, double* gtab) {
+// One kernel per range of L (items sorted by L at plan time): a kernel's register
+// count is the maximum over the L it instantiates, so short series get full occupancy.
+template <int LMIN, int LMAX>
+__global__ void __launch_bounds__(128) group_kernel(const double* __restrict__ xg, int gs, int N,
+                                                    const int32_t* __restrict__ gku, const int64_t* __restrict__ goff,
+                                                    const long long* __restrict__ items, int64_t nitems,
+                                                    const double* gtab_in, double* gtab) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nitems;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -127,7 +131,7 @@ __global__ void group_kernel(const double* __restrict__ xg, int gs, int N, const
     const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
     double* T = gtab + goff[g];
     long long* ids_out = gtab_in != gtab ? reinterpret_cast<long long*>(T + L + U * L) : nullptr;
-    group_item_dispatch<1>(L, xg, gs, ids, U, i, T, ids_out);
+    group_item_dispatch<LMIN, LMAX>(L, xg, gs, ids, U, i, T, ids_out);
   }
 }
 
@@ -393,10 +397,19 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 }
 
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
-                          const long long* items, int64_t nitems, const double* gtab_in, double* gtab_out,
-                          cudaStream_t s) {
-  if (nitems <= 0) return cudaSuccess;
-  group_kernel<<<grid_for(nitems, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
+                          const long long* items, const int64_t* item_split, const double* gtab_in,
+                          double* gtab_out, cudaStream_t s) {
+  // item_split[0..3]: item ranges with L in [1, 8], [9, 16], [17, 32]
+  const int64_t a = item_split[0], b = item_split[1], c = item_split[2], d = item_split[3];
+  if (b > a)
+    group_kernel<1, 8><<<grid_for(b - a, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items + a, b - a, gtab_in,
+                                                                   gtab_out);
+  if (c > b)
+    group_kernel<9, 16><<<grid_for(c - b, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items + b, c - b, gtab_in,
+                                                                    gtab_out);
+  if (d > c)
+    group_kernel<17, STTSV_MAX_RANK><<<grid_for(d - c, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items + c,
+                                                                                 d - c, gtab_in, gtab_out);
   return cudaGetLastError();
 }
 

@@ -56,7 +56,7 @@ def test_bench_single_gpu_contract():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
-    assert d["gpu_launches"] in (5 * 3, 5 * 4)          # prologue, [group table], edge kernel, expand
+    assert d["gpu_launches"] % 5 == 0 and 15 <= d["gpu_launches"] <= 30   # prologue, [group tables], edge, expand
     rf = d["roofline"]
     assert rf["frac"] == pytest.approx(max(rf["binding"]["hbm_stream_frac"], rf["binding"]["fp64_frac"]))
     ref = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
