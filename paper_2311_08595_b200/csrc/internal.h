@@ -132,7 +132,7 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 // plan's table (its prefix ids); gtab_out receives A, C (and the ids when it is a
 // batch vector's copy)
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
-                          const long long* items, const int64_t* item_split, const double* gtab_in,
+                          const long long* items, int64_t nitems, int lmax, const double* gtab_in,
                           double* gtab_out, cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)

@@ -114,8 +114,8 @@ __device__ __forceinline__ void group_item_dispatch(int L_rt, const double* xg, 
   }
 }
 
-// One kernel per range of L (items sorted by L at plan time): a kernel's register
-// count is the maximum over the L it instantiates, so short series get full occupancy.
+// Instantiated up to the plan's largest L (launch_groups): a kernel's register count is
+// the maximum over the L it instantiates, so plans with short series get full occupancy.
 template <int LMIN, int LMAX>
 __global__ void __launch_bounds__(128) group_kernel(const double* __restrict__ xg, int gs, int N,
                                                     const int32_t* __restrict__ gku, const int64_t* __restrict__ goff,
@@ -397,19 +397,18 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 }
 
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
-                          const long long* items, const int64_t* item_split, const double* gtab_in,
+                          const long long* items, int64_t nitems, int lmax, const double* gtab_in,
                           double* gtab_out, cudaStream_t s) {
-  // item_split[0..3]: item ranges with L in [1, 8], [9, 16], [17, 32]
-  const int64_t a = item_split[0], b = item_split[1], c = item_split[2], d = item_split[3];
-  if (b > a)
-    group_kernel<1, 8><<<grid_for(b - a, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items + a, b - a, gtab_in,
-                                                                   gtab_out);
-  if (c > b)
-    group_kernel<9, 16><<<grid_for(c - b, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items + b, c - b, gtab_in,
-                                                                    gtab_out);
-  if (d > c)
-    group_kernel<17, STTSV_MAX_RANK><<<grid_for(d - c, 128, 8192), 128, 0, s>>>(xg, gs, N, gku, goff, items + c,
-                                                                                 d - c, gtab_in, gtab_out);
+  // one launch, instantiated up to the plan's largest L (a kernel's register count is
+  // the maximum over the L it instantiates: 72 / 134 / 254 for L <= 8 / 16 / 32)
+  if (nitems <= 0) return cudaSuccess;
+  const int g = grid_for(nitems, 128, 8192);
+  if (lmax <= 8)
+    group_kernel<1, 8><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
+  else if (lmax <= 16)
+    group_kernel<1, 16><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
+  else
+    group_kernel<1, STTSV_MAX_RANK><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
   return cudaGetLastError();
 }
 

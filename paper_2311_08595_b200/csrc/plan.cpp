@@ -216,6 +216,8 @@ static double dp_fma_prefix(int N, int k, int U) {
   return f + (L + 1) + 1 + M;
 }
 
+constexpr int64_t kMemoMinEdges = (int64_t)1 << 22;  // shared-prefix memo for plans of >= 4.2 M edges
+
 // ------------------------------------------------------------------- plans
 struct sttsv_plan_s {
   int device = 0;
@@ -270,7 +272,7 @@ struct sttsv_plan_s {
   const int32_t* d_gku = nullptr;  // per prefix group: k | U << 8 (group_kernel)
   const int64_t* d_goff = nullptr;  // per prefix group: offset of its record in the group table
   const long long* d_items = nullptr;  // group_kernel work items
-  int64_t item_split[4] = {0, 0, 0, 0};  // item ranges by L (group_kernel instantiations)
+  int group_lmax = 0;                    // largest L among the prefix groups
   int64_t nitems = 0;
   int64_t prefix_tiles = 0, prefix_groups = 0, prefix_inc = 0;
   // edge-kernel timing (sttsv_plan_profile)
@@ -496,8 +498,14 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   const int nblk = p->ent.consumers / 32, wblk = tile / nblk;
   std::vector<int> wuni(N + 1, 0);
   std::vector<double> wconst(N + 1, 0.0);
+  // The memo pays once the stream is long enough to amortise its group-table kernel and
+  // per-block control work: measured on B200, mid (1e6 edges) runs faster without it and
+  // high-rank (5e6) faster with it; below kMemoMinEdges a plan uses the plain per-edge path
+  // (STTSV_MEMO_MIN_EDGES overrides, for experiments).
+  int64_t memo_min = kMemoMinEdges;
+  if (const char* env = getenv("STTSV_MEMO_MIN_EDGES")) memo_min = atoll(env);
   const bool memo = p->ent.prefix_mmax > 0 && !(flags & (STTSV_DETERMINISTIC | STTSV_NO_PREFIX_MEMO)) &&
-                    !getenv("STTSV_NO_PREFIX");
+                    !getenv("STTSV_NO_PREFIX") && p->local_edges >= memo_min;
   // Sort each bucket lexicographically (stable: the plan is deterministic).
   // Consecutive edges then share their hot low slots, which the kernel's
   // per-lane run accumulators turn into one deposit per run.
@@ -699,18 +707,8 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
       }
     }
     p->prefix_groups = (int64_t)h_gku.size();
-    // group_kernel instantiations by L range (kernels.cu): items sorted by L
-    auto Lof = [&](long long it) { return N - (h_gku[(size_t)(it >> 8)] & 255) + 1; };
-    std::stable_sort(h_items.begin(), h_items.end(), [&](long long a, long long b) { return Lof(a) < Lof(b); });
-    int64_t c8 = 0, c16 = 0;
-    for (long long it : h_items) {
-      c8 += Lof(it) <= 8;
-      c16 += Lof(it) <= 16;
-    }
-    p->item_split[0] = 0;
-    p->item_split[1] = c8;
-    p->item_split[2] = c16;
-    p->item_split[3] = (int64_t)h_items.size();
+    // the group kernel is instantiated up to the largest L of the plan's groups (kernels.cu)
+    for (int32_t gk : h_gku) p->group_lmax = std::max(p->group_lmax, N - (gk & 255) + 1);
   }
   kp.n_active = (int32_t)na;
   kp.T = T;
@@ -945,9 +943,7 @@ extern "C" int sttsv_apply_launches(sttsv_plan_t p) {
   int l = 0;
   if (p->n_active > 0) l += 2;          // gather + expand
   if (p->kp.num_tiles > 0) l += 1;      // edge kernel
-  if (p->kp.gtab)                       // shared-prefix group table (one kernel per L range)
-    l += (p->item_split[1] > p->item_split[0]) + (p->item_split[2] > p->item_split[1]) +
-         (p->item_split[3] > p->item_split[2]);
+  if (p->kp.gtab) l += 1;               // shared-prefix group table
   if (p->det) l += 2;                   // deterministic chunk + vertex sums
   return l;
 }
@@ -1006,8 +1002,8 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
     }
     const bool groups = p->kp.gtab != nullptr;
     if (groups)  // per-apply shared-prefix group table (prefix.cuh)
-      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->d_items, p->item_split, p->kp.gtab,
-                             const_cast<double*>(p->kp.gtab), s), "group kernel launch");
+      CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->d_items, p->nitems, p->group_lmax,
+                             p->kp.gtab, const_cast<double*>(p->kp.gtab), s), "group kernel launch");
     CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed || groups),
              "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
@@ -1257,7 +1253,7 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       if (groups) {
         for (int v = 0; v < nvec; ++v)
           CUDA_TRY(launch_groups(p->b_xg + (size_t)v * na * p->gs, p->gs, p->N, p->d_gku, p->d_goff, p->d_items,
-                                 p->item_split, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles, s),
+                                 p->nitems, p->group_lmax, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles, s),
                    "group kernel launch");
         kp.gtab = p->b_gtab;
         kp.gtab_vstride = p->gtab_doubles;

@@ -8,6 +8,12 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# Parity tests exercise the shared-prefix memo on every input, however small (the
+# library enables it only for plans of >= 2^22 edges by default, plan.cpp
+# kMemoMinEdges); the full-size tests restore the production threshold.
+os.environ.setdefault("STTSV_MEMO_MIN_EDGES", "0")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")

@@ -34,7 +34,8 @@ def test_bench_torchrun_world2_no_comm():
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "5", "--warmup", "3", "--config", "mid", "--no-comm",
            "--no-merge-report", "--no-batch-report", "--no-memo-report", "--cpu-seconds", "1"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    env = {k: v for k, v in os.environ.items() if k != "STTSV_MEMO_MIN_EDGES"}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["steps"] == 5 and d["config"]["workload"] == "mid"
@@ -50,7 +51,8 @@ def test_bench_single_gpu_contract():
     driver reads are present and consistent."""
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "5", "--warmup", "3", "--config", "mid",
            "--no-merge-report", "--no-batch-report", "--no-memo-report", "--cpu-seconds", "1"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    env = {k: v for k, v in os.environ.items() if k != "STTSV_MEMO_MIN_EDGES"}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     d = _last_json(r.stdout)
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",

@@ -34,6 +34,12 @@ HOT_TOL = 1e-12
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
+@pytest.fixture(autouse=True)
+def production_thresholds(monkeypatch):
+    """The bench's launch configuration: the library's own memo threshold."""
+    monkeypatch.delenv("STTSV_MEMO_MIN_EDGES", raising=False)
+
+
 @pytest.fixture(scope="module")
 def torch_cuda():
     import torch
