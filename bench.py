@@ -61,17 +61,23 @@ def fp64_peak_tflops():
     return 37.2, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
 
 
-def ncu_traffic(config):
-    """dram bytes per edge-kernel launch from the committed ncu --set full summary, if any."""
+def ncu_summary(config):
+    """The committed ncu --set full summary of the edge kernel (profiles/ncu_edge_kernel.json)
+    for this config, if any: DRAM bytes and warp instructions per launch."""
     p = os.path.join(ROOT, "profiles", "ncu_edge_kernel.json")
     try:
         with open(p) as f:
             d = json.load(f)
         if d.get("config") == config:
-            return d.get("dram_bytes_per_launch")
+            return d
     except Exception:
         pass
-    return None
+    return {}
+
+
+def ncu_traffic(config):
+    """dram bytes per edge-kernel launch from the committed ncu --set full summary, if any."""
+    return ncu_summary(config).get("dram_bytes_per_launch")
 
 
 # ------------------------------------------------------------------ clocks
@@ -383,17 +389,38 @@ def run_ours(args):
     fp64_tf = 2.0 * info["fma_executed"] / ksec / 1e12     # FP64 operations the kernel executes
     stream_frac, fp64_frac = stream_gbs / peak, fp64_tf / fp64_peak
     traffic = ncu_traffic(args.config)
-    if stream_frac >= fp64_frac:
+    # instruction issue: warp instructions per launch (committed ncu summary of this
+    # kernel on this config) / live kernel time, against 148 SMs x 4 schedulers x 1
+    # warp-instruction per clock at the sampled SM clock
+    nsum = ncu_summary(args.config)
+    issue = None
+    if nsum.get("smsp__inst_executed.sum"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk = (sampler.summary().get("sm_mhz") or 1965.0) * 1e6
+        ipeak = sms * 4 * clk
+        iach = nsum["smsp__inst_executed.sum"] / ksec
+        issue = {"achieved": iach, "peak": ipeak, "unit": "warp-inst/s", "frac": iach / ipeak,
+                 "warp_inst_per_launch": nsum["smsp__inst_executed.sum"],
+                 "source": "profiles/ncu_edge_kernel.json (%s)" % nsum.get("report", "")}
+    issue_frac = issue["frac"] if issue else 0.0
+    if stream_frac >= max(fp64_frac, issue_frac):
         head = {"bound": "hbm", "achieved": stream_gbs, "peak": peak, "unit": "GB/s", "frac": stream_frac}
-    else:
+    elif fp64_frac >= issue_frac:
         head = {"bound": "alu", "achieved": fp64_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": fp64_frac}
+    else:
+        head = {"bound": "alu", "achieved": issue["achieved"], "peak": issue["peak"], "unit": "warp-inst/s",
+                "frac": issue_frac}
     roofline = dict(head)
     roofline.update({
         "traffic": traffic, "kernel": "sttsv::edge_kernel<N>", "kernel_ms": kern_avg,
         "kernel_share_of_step": kern_avg / ms_step,
-        "binding": {"frac": max(stream_frac, fp64_frac), "hbm_stream_frac": stream_frac, "fp64_frac": fp64_frac,
-                    "note": "primary figure: the larger of the two roofs the kernel is held to; 'alu' = the "
-                            "FP64 DFMA pipe"},
+        "binding": {"frac": max(stream_frac, fp64_frac, issue_frac), "hbm_stream_frac": stream_frac,
+                    "fp64_frac": fp64_frac, "issue_frac": issue_frac if issue else None,
+                    "note": "primary figure: the largest of the roofs the kernel is held to — HBM on the bytes it "
+                            "streams, the FP64 DFMA pipe on the FP64 operations it executes, instruction issue "
+                            "on the warp instructions it executes (the shared-prefix memo leaves mostly "
+                            "control work: issue is the binding roof on large)"},
+        "issue": issue,
         "stream": {"id_bytes": info["id_bytes"], "bytes_per_launch": phys_bytes, "gbs": stream_gbs,
                    "frac": stream_frac, "peak_source": peak_src,
                    "note": "bytes the kernel streams: plan_info stream_bytes (uint16 ids when n_active <= 65536; no "

@@ -210,6 +210,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+
+// consumer-side wait: spin (default) or, with STTSV_CONSUMER_HINT, a suspend-time-hinted
+// try_wait like the producer's (the waiting warp stops taking issue slots)
+#ifndef STTSV_CONSUMER_HINT
+#define STTSV_CONSUMER_HINT 0
+#endif
+__device__ __forceinline__ void mbar_wait_consumer(uint64_t* bar, uint32_t parity) {
+#if STTSV_CONSUMER_HINT
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(STTSV_CONSUMER_HINT)
+        : "memory");
+    if (ok) return;
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 // producer-side wait: try_wait with a suspend-time hint, so the waiting thread
 // sleeps in hardware until the phase completes (or the hint expires) instead of
 // spinning and stealing issue slots from the consumers
@@ -1166,7 +1190,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       mbar_wait(&full[s], (uint32_t)((it / SLOTS) & 1));
       wait_cyc += clock64() - w0;
 #else
-      mbar_wait(&full[s], (uint32_t)((it / SLOTS) & 1));
+      mbar_wait_consumer(&full[s], (uint32_t)((it / SLOTS) & 1));
 #endif
       const int64_t t = stile[s];
       if (t < 0) break;

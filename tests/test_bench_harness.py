@@ -60,7 +60,9 @@ def test_bench_single_gpu_contract():
         assert k in d, k
     assert d["gpu_launches"] % 5 == 0 and 15 <= d["gpu_launches"] <= 30   # prologue, [group tables], edge, expand
     rf = d["roofline"]
-    assert rf["frac"] == pytest.approx(max(rf["binding"]["hbm_stream_frac"], rf["binding"]["fp64_frac"]))
+    b = rf["binding"]
+    assert rf["frac"] == pytest.approx(b["frac"])
+    assert b["frac"] == pytest.approx(max(b["hbm_stream_frac"], b["fp64_frac"], b["issue_frac"] or 0.0))
     ref = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                           "--warmup", "0", "--config", "mid"], capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert ref.returncode == 0, ref.stderr[-3000:]
