@@ -120,7 +120,7 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 // shared-prefix memo (prefix.cuh): a tile whose edges share a prefix of U members
 // runs the DP over its M = K - U own members, M <= PREFIX_MMAX
 #ifndef STTSV_PREFIX_MMAX
-#define STTSV_PREFIX_MMAX 4
+#define STTSV_PREFIX_MMAX 6
 #endif
 #ifndef STTSV_PREFIX_MMAX_BIG
 #define STTSV_PREFIX_MMAX_BIG 8
