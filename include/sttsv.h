@@ -218,6 +218,10 @@ typedef struct {
   int64_t prefix_groups;   /* runs of consecutive such blocks with the same prefix                 */
   int64_t prefix_incidences; /* incidences that lie in a shared prefix                            */
   int64_t num_tiles;       /* tiles of the edge stream                                            */
+  int64_t m0_edges;        /* edges in warp blocks of one repeated vertex set (M = 0): not in the tile
+                              stream; their prefix members get C_i[0] x (sum of w') per apply     */
+  int64_t m0_groups;       /* distinct vertex sets of those blocks                                */
+  int64_t m0_chunks;       /* chunks of their stored weights summed per apply (non-uniform weights) */
 } sttsv_plan_info_t;
 
 sttsv_status_t sttsv_plan_info(sttsv_plan_t plan, sttsv_plan_info_t* info);

@@ -62,4 +62,12 @@ extern "C" int sttsv_debug_kcycles(unsigned long long out[2 * (STTSV_MAX_RANK + 
   }
   return 0;
 }
+extern "C" int sttsv_debug_cta(unsigned long long out[3 * 1024], int reset) {
+  cudaMemcpyFromSymbol(out, sttsv::g_cta_ns, sizeof(unsigned long long) * 3 * 1024);
+  if (reset) {
+    static unsigned long long z[3 * 1024] = {0};
+    cudaMemcpyToSymbol(sttsv::g_cta_ns, z, sizeof(z));
+  }
+  return 0;
+}
 #endif

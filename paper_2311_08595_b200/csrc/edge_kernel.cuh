@@ -59,7 +59,16 @@ constexpr unsigned kFull = 0xffffffffu;
 #if STTSV_WAITPROF
 __device__ unsigned long long g_wait_cycles[4];
 __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per bucket k: cycles, tiles
+// per CTA: globaltimer at the consumers' start, at the CTA's end, and its tile count
+__device__ unsigned long long g_cta_ns[3 * 1024];
 #endif
+// STTSV_WAITPROF == 3: g_k_cycles is indexed by block class instead of k:
+// 0 = M = 0 block, M = 1..8 own members, 20 + k = full DP (no shared prefix)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 
 // ---- compile-time tuning (each default was chosen by A/B timing on B200 with
@@ -91,6 +100,23 @@ __device__ unsigned long long g_k_cycles[2 * (STTSV_MAX_RANK + 1)];  // per buck
 // N = 11 .. BIG_MIN-1: one CTA per SM with 11 consumer warps (168 registers, no spills)
 #ifndef STTSV_MID_BLOCKS
 #define STTSV_MID_BLOCKS 1
+#endif
+// consumer warps take the warp blocks of the staged tiles from a per-CTA counter
+// (block g = tile iteration g / NCW, block g % NCW), so a warp held up by an
+// expensive block does not hold the others back (0: warp w always takes block w)
+#ifndef STTSV_DYN_BLOCKS
+#define STTSV_DYN_BLOCKS 1
+#endif
+// software-pipelined queue loop of the shared-prefix blocks for M*L <= PIPE_ML
+// (the next entry's rows in flight during the current DP; more costs registers)
+#ifndef STTSV_PIPE_ML
+#define STTSV_PIPE_ML 8
+#endif
+#ifndef STTSV_SLOTS
+#define STTSV_SLOTS 16
+#endif
+#ifndef STTSV_RING_KB_MID
+#define STTSV_RING_KB_MID 220
 #endif
 #ifndef STTSV_NCW_MID
 #define STTSV_NCW_MID 11
@@ -159,7 +185,7 @@ struct EdgeCfg {
   static constexpr int RED_BYTES = NCW_PREF * SCR_DOUBLES * 8;
   // (the large-rank path runs one CTA per SM: its reduction rows come on top)
   static constexpr int RING_BUDGET = BIG ? (STTSV_BIG_LOCAL ? 96 : 48) * 1024
-                                         : (N <= 10 ? STTSV_RING_KB : 220 / STTSV_MID_BLOCKS) * 1024 - RED_BYTES;
+                                         : (N <= 10 ? STTSV_RING_KB : STTSV_RING_KB_MID / STTSV_MID_BLOCKS) * 1024 - RED_BYTES;
   // consumer warps per CTA (NCW_PREF), fewer when two stages of the largest
   // bucket would not fit the ring budget
   static constexpr int NCW_FIT = RING_BUDGET / (2 * 32 * EPL * EDGE_BYTES);
@@ -172,7 +198,7 @@ struct EdgeCfg {
   // byte ring: a stage takes TILE*(4k+8) bytes of its bucket's k, so small-k
   // tiles are more deep in flight; SLOTS bounds the stages in flight
   static constexpr int RING_BYTES = (STAGES * STAGE_BYTES > RING_BUDGET ? STAGES * STAGE_BYTES : RING_BUDGET) / 128 * 128;
-  static constexpr int SLOTS = 16;
+  static constexpr int SLOTS = STTSV_SLOTS;
   static constexpr int RMAX = BIG ? 4 : (KMAX < 8 ? KMAX : 8);  // slots with a register run accumulator
   static constexpr int MIN_BLOCKS = BIG ? 1 : (N <= 10 ? STTSV_MIN_BLOCKS : STTSV_MID_BLOCKS);
   static constexpr bool BIG_PREFIX = BIG && PMAX > 0;
@@ -485,6 +511,50 @@ __device__ __forceinline__ void prefix_tile_flush(double (&sb)[L], double* sred,
   }
 }
 
+// prefix_tile_flush with the prefix members' rows prefetched at the start of the
+// block (lane i < U holds C_i in c[] and the member's id in v; U <= 31 here): the
+// flush does not wait on the group table
+template <int L>
+__device__ __forceinline__ void prefix_tile_flush_pre(double (&sb)[L], double* sred, const double (&c)[L], int v,
+                                                      const Sink& sk, int lane) {
+  if constexpr (L <= 2) {
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sb[j] += __shfl_xor_sync(kFull, sb[j], o);
+    if (v >= 0) {
+      double d = 0.0;
+#pragma unroll
+      for (int j = 0; j < L; ++j) d = fma(c[j], sb[j], d);
+      red_add(sk.at(v), d);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < L; ++j) sred[j * kRedStride + lane] = sb[j];
+    __syncwarp();
+    double t = 0.0;
+    if (lane < L) {
+      const double2* r = reinterpret_cast<const double2*>(sred + lane * kRedStride);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 u = r[q];
+        t += u.x;
+        t += u.y;
+      }
+    }
+    __syncwarp();
+    if (lane < L) sred[lane] = t;
+    __syncwarp();
+    if (v >= 0) {
+      double d = 0.0;
+#pragma unroll
+      for (int j = 0; j < L; ++j) d = fma(c[j], sred[j], d);
+      red_add(sk.at(v), d);
+    }
+    __syncwarp();
+  }
+}
+
 // M = 0 tile or edge block (every edge the same vertex set): the prefix members
 // get sum w' times C_i[0]; with uniform weights the sum is wc x (real edges in
 // positions [base, base + n)), no loads at all
@@ -530,6 +600,17 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
     double a[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) a[j] = __ldg(G + j);  // front A (row format), the same on every lane
+    // the flush's rows: lane i < U takes prefix member i's C_i and id now (U <= 31)
+    double cpre[L];
+    int vpre = -1;
+    if (lane < U) {
+#pragma unroll
+      for (int j = 0; j < L; ++j) cpre[j] = __ldg(G + L + lane * L + j);
+      vpre = (int)__ldg(reinterpret_cast<const long long*>(G + L + U * L) + lane);
+    } else {
+#pragma unroll
+      for (int j = 0; j < L; ++j) cpre[j] = 0.0;
+    }
     // Runs of identical consecutive edges among the lane's EPL edges (sorted
     // buckets keep duplicates adjacent) need one DP each, on the run's summed
     // weight: pass 1 counts the lane's runs, a warp scan places them in this
@@ -590,18 +671,9 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
     }
     __syncwarp();
     const int c = (Q + 31) >> 5;
-#pragma unroll 1
-    for (int e = lane * c; e < lane * c + c; ++e) {
-      const bool live = e < Q;
-      const int col = qc[live ? e : 0];
-      const double w = live ? qw[e] : 0.0;
-      int id[M];
-      double h[M][L];
-#pragma unroll
-      for (int i = 0; i < M; ++i) {
-        id[i] = (int)sids[i * TILE + col];
-        load_series<L>(xg + (size_t)(uint32_t)id[i] * GS, h[i]);
-      }
+    // one queue entry: the DP over the own members with the front A, the
+    // deposits of the own members and the entry's SB term
+    auto entry = [&](bool live, double w, const int (&id)[M], const double (&h)[M][L]) {
       double q[M], F, bh[L];
       dp_front_norm<M, L>(a, h, q, F, bh);
       const double wF = w * F;
@@ -613,9 +685,53 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
       sb[0] += cw;
 #pragma unroll
       for (int j = 1; j < L; ++j) sb[j] = fma(cw, bh[j], sb[j]);
+    };
+    auto fetch = [&](int e, bool& live, double& w, int (&id)[M], double (&h)[M][L]) {
+      live = e < Q;
+      const int col = qc[live ? e : 0];
+      w = live ? qw[e] : 0.0;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        id[i] = (int)sids[i * TILE + col];
+        load_series<L>(xg + (size_t)(uint32_t)id[i] * GS, h[i]);
+      }
+    };
+    if constexpr (M * L <= STTSV_PIPE_ML) {
+      // software pipeline: the next entry's ids and table rows are loaded before
+      // the current entry's DP (the row loads are a round's latency)
+      bool liven;
+      double wn;
+      int idn[M];
+      double hn[M][L];
+      fetch(lane * c, liven, wn, idn, hn);
+#pragma unroll 1
+      for (int e = lane * c; e < lane * c + c; ++e) {
+        const bool live = liven;
+        const double w = wn;
+        int id[M];
+        double h[M][L];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          id[i] = idn[i];
+#pragma unroll
+          for (int j = 0; j < L; ++j) h[i][j] = hn[i][j];
+        }
+        if (e + 1 < lane * c + c) fetch(e + 1, liven, wn, idn, hn);
+        entry(live, w, id, h);
+      }
+    } else {
+#pragma unroll 1
+      for (int e = lane * c; e < lane * c + c; ++e) {
+        bool live;
+        double w;
+        int id[M];
+        double h[M][L];
+        fetch(e, live, w, id, h);
+        entry(live, w, id, h);
+      }
     }
     __syncwarp();  // the queue is read before the reduction reuses the scratch
-    prefix_tile_flush<L>(sb, sred, G, U, sk, lane);
+    prefix_tile_flush_pre<L>(sb, sred, cpre, vpre, sk, lane);
   }
 }
 
@@ -1047,10 +1163,18 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
   __shared__ uint8_t su[SLOTS];     // its staged prefix length U_stage (id columns 0..U_stage-1 are not staged)
   __shared__ long long sblk[SLOTS][NCW];  // per warp block: (group record offset << 8) | U (prefix.cuh)
   __shared__ uint8_t sbk[SLOTS];    // its bucket (index into p.b)
+  __shared__ int64_t sit[SLOTS];    // the producer iteration staged in each slot (dynamic blocks)
+  __shared__ unsigned int s_next;   // next warp block of the CTA's staged sequence (dynamic blocks)
 
   for (int j = tid; j < p.H * nvec; j += Cfg::THREADS) priv_cta[j] = 0.0;
+#if STTSV_WAITPROF > 1
+  __shared__ unsigned long long s_kc[2 * (STTSV_MAX_RANK + 1)];  // per-CTA class counters (one global add each at the end)
+  for (int j = tid; j < 2 * (STTSV_MAX_RANK + 1); j += Cfg::THREADS) s_kc[j] = 0ull;
+#endif
   if (tid == 0) {
+    s_next = 0u;
     for (int s = 0; s < SLOTS; ++s) {
+      sit[s] = -1;
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
@@ -1115,6 +1239,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         const uint32_t off = (uint32_t)(start % Cfg::RING_BYTES);
         soff[s] = off;
         stile[s] = t;
+        sit[s] = it;
         su[s] = (uint8_t)tu;
         sbk[s] = (uint8_t)b;
 #pragma unroll
@@ -1181,20 +1306,45 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
 #if STTSV_WAITPROF
     long long wait_cyc = 0;
     const long long c_start = clock64();
+    if (tid == 0 && blockIdx.x < 1024) g_cta_ns[3 * blockIdx.x] = gtimer();
+    unsigned long long ntiles = 0;
+#endif
+#if !STTSV_DYN_BLOCKS
+    const int wb = warp;  // this warp's block of every tile
 #endif
     for (int64_t it = 0;; ++it) {
+#if STTSV_DYN_BLOCKS
+      // the next block of the CTA's sequence.  Its tile may be more than one
+      // phase ahead of the slot's barrier (the slot's previous tile not yet
+      // staged), where a parity wait would pass on the older phase: the warp
+      // first waits until the producer has published this iteration in the slot
+      // (then the barrier is in this iteration's phase) and then on the barrier
+      unsigned int gblk = 0u;
+      if (lane == 0) gblk = atomicAdd(&s_next, 1u);
+      gblk = __shfl_sync(kFull, gblk, 0);
+      it = (int64_t)(gblk / NCW);
+      const int wb = (int)(gblk % NCW);
+#endif
       const int s = (int)(it % SLOTS);
-      const int base = warp * 32 * EPL;
+      const int base = wb * 32 * EPL;
 #if STTSV_WAITPROF
       const long long w0 = clock64();
-      mbar_wait(&full[s], (uint32_t)((it / SLOTS) & 1));
-      wait_cyc += clock64() - w0;
+#endif
+#if STTSV_DYN_BLOCKS
+      while (*(volatile int64_t*)&sit[s] != it) __nanosleep(32);
+      mbar_wait_consumer(&full[s], (uint32_t)((it / SLOTS) & 1));
 #else
       mbar_wait_consumer(&full[s], (uint32_t)((it / SLOTS) & 1));
+#endif
+#if STTSV_WAITPROF
+      wait_cyc += clock64() - w0;
 #endif
       const int64_t t = stile[s];
       if (t < 0) break;
       any = true;
+#if STTSV_WAITPROF
+      ++ntiles;
+#endif
       const int b = sbk[s];
       const int k = p.b[b].k;
 #if STTSV_WAITPROF > 1
@@ -1203,7 +1353,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       const DetSink ds{DET ? p.slot + p.b[b].ids_off + (t - p.b[b].tile_begin) * TILE : nullptr, p.b[b].stride,
                        p.contrib};
       const int us = su[s];                 // staged from column us
-      const long long bh = sblk[s][warp];   // this warp's block: shared prefix length and group
+      const long long bh = sblk[s][wb];     // this warp's block: shared prefix length and group
       const int tu = (int)(bh & 255);
       const int64_t goff = bh >> 8;
       {
@@ -1219,7 +1369,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
           if (tu > 0 && tu == k && !DET) {
             // M = 0: every edge of the warp's block is the same vertex set
             const int nb = Cfg::BIG ? 32 : 32 * EPL;
-            const int bb = Cfg::BIG ? warp * 32 : base;
+            const int bb = Cfg::BIG ? wb * 32 : base;
             double part = 0.0;
             if (sw.uni) {
               int n = sw.real - bb;
@@ -1239,6 +1389,12 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
             }
             pend_w += part;
             __syncwarp();
+#if STTSV_WAITPROF == 3
+            if (lane == 0) {
+              atomicAdd(&s_kc[0], (unsigned long long)(clock64() - kc0));
+              atomicAdd(&s_kc[1], 1ull);
+            }
+#endif
             if (lane == 0) mbar_arrive(&empty[s]);
             continue;
           }
@@ -1263,16 +1419,16 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
             }
             if (!done) dispatch_k<N, 1, TILE, EPL, RMAX, DET, IdT>(k, sids, sw, base, xgv, ra, skv, ds, lane);
           } else {
-            const int col = warp * 32 + lane;  // EPL = 1
+            const int col = wb * 32 + lane;  // EPL = 1
             if constexpr (Cfg::BIG_PREFIX && !DET) {
               if (tu > 0) {  // shared-prefix tile (prefix.cuh); warp-uniform
                 need_groups();
 #if STTSV_BIG_LOCAL
                 dispatch_big_prefix<1, KMAX, TILE, 1, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col), sw,
-                                                            warp * 32, Gv, xgv, p.gs, lstk, ra, skv, sred, lane);
+                                                            wb * 32, Gv, xgv, p.gs, lstk, ra, skv, sred, lane);
 #else
                 dispatch_big_prefix<1, KMAX, TILE, NCW * 32, RMAX>(p.N - k + 1, k, tu, sids + col, sw.at(col, col),
-                                                                   sw, warp * 32, Gv, xgv, p.gs,
+                                                                   sw, wb * 32, Gv, xgv, p.gs,
                                                                    stack + (warp * 32 + lane), ra, skv, sred, lane);
 #endif
                 done = true;
@@ -1301,8 +1457,9 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       __syncwarp();
 #if STTSV_WAITPROF > 1
       if (lane == 0) {
-        atomicAdd(&g_k_cycles[2 * k], (unsigned long long)(clock64() - kc0));
-        atomicAdd(&g_k_cycles[2 * k + 1], 1ull);
+        const int cls = STTSV_WAITPROF == 3 ? (tu == 0 ? 20 + (k < 12 ? k : 12) : k - tu) : k;
+        atomicAdd(&s_kc[2 * cls], (unsigned long long)(clock64() - kc0));
+        atomicAdd(&s_kc[2 * cls + 1], 1ull);
       }
 #endif
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -1312,6 +1469,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
       atomicAdd(&g_wait_cycles[0], (unsigned long long)wait_cyc);
       atomicAdd(&g_wait_cycles[1], (unsigned long long)(clock64() - c_start));
       atomicAdd(&g_wait_cycles[2], 1ull);
+      if (warp == 0 && blockIdx.x < 1024) g_cta_ns[3 * blockIdx.x + 2] = ntiles;
     }
 #endif
     if (pend_goff >= 0) flush_pending();
@@ -1331,6 +1489,13 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
     const double v = __ldcg(priv_cta + j);
     if (v != 0.0) red_add(p.ya + (size_t)(j / p.H) * p.ya_vstride + j % p.H, v);
   }
+#if STTSV_WAITPROF
+  if (tid == 0 && blockIdx.x < 1024) g_cta_ns[3 * blockIdx.x + 1] = gtimer();
+#endif
+#if STTSV_WAITPROF > 1
+  for (int j = tid; j < 2 * (STTSV_MAX_RANK + 1); j += Cfg::THREADS)
+    if (s_kc[j]) atomicAdd(&g_k_cycles[j], s_kc[j]);
+#endif
   // the last CTA to finish resets the scheduler counters for the next launch
   // (every producer has stopped taking tiles once all CTAs have counted in)
   if (tid == 0) {

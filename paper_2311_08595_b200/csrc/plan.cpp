@@ -275,6 +275,15 @@ struct sttsv_plan_s {
   int group_lmax = 0;                    // largest L among the prefix groups
   int64_t nitems = 0;
   int64_t prefix_tiles = 0, prefix_groups = 0, prefix_inc = 0;
+  // M = 0 runs (prefix.cuh): edges whose warp block is one vertex set leave the tile
+  // stream; group_kernel deposits C_i[0] * t0 with t0 = m0w[g] (uniform-weight
+  // buckets: w' x edges) + the group's chunk sums of the stored weights (m0sum_kernel)
+  int64_t m0_edges = 0, m0_groups = 0, m0_chunks = 0;
+  const double* d_gm0w = nullptr;     // per group: the uniform-weight part of t0
+  const int64_t* d_gcoff = nullptr;   // per group: its chunks gcoff[g] .. gcoff[g+1]
+  const long long* d_m0chunk = nullptr;  // per chunk: (first weight << 13) | length
+  const double* d_w0 = nullptr;       // the M = 0 edges' weights of non-uniform buckets
+  double* d_m0sum = nullptr;          // per chunk: its weight sum (per apply)
   // edge-kernel timing (sttsv_plan_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
@@ -506,6 +515,16 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (const char* env = getenv("STTSV_MEMO_MIN_EDGES")) memo_min = atoll(env);
   const bool memo = p->ent.prefix_mmax > 0 && !(flags & (STTSV_DETERMINISTIC | STTSV_NO_PREFIX_MEMO)) &&
                     !getenv("STTSV_NO_PREFIX") && p->local_edges >= memo_min;
+  struct M0Run {
+    int k;
+    int64_t ids;     // offset of its vertex set in m0ids
+    int64_t cnt;     // edges
+    int64_t w0, w1;  // its weights in h_w0 (non-uniform buckets)
+  };
+  std::vector<M0Run> m0runs;
+  std::vector<int32_t> m0ids;
+  std::vector<double> h_w0;
+  std::vector<int64_t> m0cnt(N + 1, 0);
   // Sort each bucket lexicographically (stable: the plan is deterministic).
   // Consecutive edges then share their hot low slots, which the kernel's
   // per-lane run accumulators turn into one deposit per run.
@@ -575,6 +594,57 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
         const bool ok = u >= 1 && (M == 0 || (M <= p->ent.prefix_mmax && L <= p->ent.prefix_lmax));
         tile_u[k][bl] = (uint8_t)(ok ? u : 0);
       }
+      // M = 0 blocks (U = k: every edge of the block is the same vertex set) leave the
+      // tile stream.  Their contribution is w' summed over the block times the group's
+      // C_i[0] (prefix.cuh); consecutive blocks of one set form one run.  Uniform-weight
+      // buckets keep the run's edge count (t0 = w' x count); otherwise the run's weights
+      // move to the M = 0 weight column that m0sum_kernel sums every apply.  The kept
+      // blocks are compacted in order and the bucket is re-padded to whole tiles.
+      std::vector<uint8_t> nu;
+      nu.reserve(tile_u[k].size());
+      int64_t nkept = 0, kreal = 0;
+      for (int64_t bl = 0; bl < ntl * nblk; ++bl) {
+        const int64_t j0 = bl * wblk;
+        const int64_t real = std::max<int64_t>(0, std::min<int64_t>(wblk, kept - j0));
+        if (real == 0) break;  // only padding from here on
+        if (tile_u[k][bl] == k) {
+          M0Run* r = m0runs.empty() ? nullptr : &m0runs.back();
+          bool same = r && r->k == k;
+          for (int q = 0; q < k && same; ++q) same = m0ids[r->ids + q] == col[(int64_t)q * st + j0];
+          if (!same) {
+            m0runs.push_back(M0Run{k, (int64_t)m0ids.size(), 0, (int64_t)h_w0.size(), (int64_t)h_w0.size()});
+            for (int q = 0; q < k; ++q) m0ids.push_back(col[(int64_t)q * st + j0]);
+            r = &m0runs.back();
+          }
+          r->cnt += real;
+          if (!wuni[k]) {
+            h_w0.insert(h_w0.end(), h_w.begin() + w_off[k] + j0, h_w.begin() + w_off[k] + j0 + real);
+            r->w1 = (int64_t)h_w0.size();
+          }
+          m0cnt[k] += real;
+          continue;
+        }
+        if (nkept != bl) {
+          for (int q = 0; q < k; ++q)
+            std::copy(col + (int64_t)q * st + j0, col + (int64_t)q * st + j0 + wblk, col + (int64_t)q * st + nkept * wblk);
+          std::copy(h_w.begin() + w_off[k] + j0, h_w.begin() + w_off[k] + j0 + wblk,
+                    h_w.begin() + w_off[k] + nkept * wblk);
+        }
+        nu.push_back(tile_u[k][bl]);
+        kreal = nkept * wblk + real;
+        ++nkept;
+      }
+      if (nkept < ntl * nblk) {
+        // re-pad: weight-0 copies of the last kept edge, full-DP blocks (U = 0)
+        const int64_t npad = (nkept + nblk - 1) / nblk * nblk * wblk;
+        for (int64_t j = kreal; j < npad; ++j) {
+          for (int q = 0; q < k; ++q) col[(int64_t)q * st + j] = col[(int64_t)q * st + kreal - 1];
+          h_w[w_off[k] + j] = 0.0;
+        }
+        while ((int64_t)nu.size() < npad / wblk) nu.push_back(0);
+        tile_u[k].swap(nu);
+        stored[k] = kreal;
+      }
     }
   }
   std::vector<int32_t>().swap(rows);
@@ -627,9 +697,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     b.wuni = wuni[k];
     b.wc = wconst[k];
     tiles += (stored[k] + tile - 1) / tile;
-    fma += dp_fma(N, k) * (double)stored[k];
-    p->stored_edges += stored[k];
-    p->stored_inc += stored[k] * k;
+    fma += dp_fma(N, k) * (double)(stored[k] + m0cnt[k]);
+    p->stored_edges += stored[k] + m0cnt[k];
+    p->stored_inc += (stored[k] + m0cnt[k]) * k;
+    p->m0_edges += m0cnt[k];
+    p->prefix_inc += m0cnt[k] * k;
+    if (!wuni[k]) p->stream_bytes += m0cnt[k] * 8;  // the M = 0 weights m0sum_kernel reads
     const int64_t ntl = (stored[k] + tile - 1) / tile;
     for (int64_t tl = 0; tl < ntl; ++tl) {
       int us = k;  // staged columns: from the smallest prefix of the tile's blocks
@@ -656,7 +729,10 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<double> h_gtab;  // group records (prefix.cuh): [A: L][C: U x L][ids: U]; ids filled here
   std::vector<long long> h_items;  // group_kernel work items: (group << 8) | prefix member
   std::map<std::vector<int32_t>, int32_t> gmap;
-  if (memo && p->prefix_tiles > 0) {
+  std::vector<double> h_gm0w;          // per group: w' x edges of its uniform-weight M = 0 runs
+  std::vector<int64_t> h_gcoff;        // per group: first chunk (+ end sentinel)
+  std::vector<long long> h_m0chunk;    // per chunk: (first weight << 13) | length
+  if (memo && (p->prefix_tiles > 0 || !m0runs.empty())) {
     h_hdr.assign((size_t)tiles * (1 + nblk), 0);
     int32_t gid = -1;
     int pk = -1, pu = -1;
@@ -705,6 +781,62 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
           h_hdr[(size_t)t * (1 + nblk) + 1 + w] = ((long long)h_goff[gid] << 8) | u;
         }
       }
+    }
+    // M = 0 runs: a group per distinct vertex set (U = k: all members are prefix members)
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> granges;  // per group: its M = 0 weight ranges
+    std::vector<long double> gm0(h_gku.size(), 0.0L);
+    granges.resize(h_gku.size());
+    for (const M0Run& r : m0runs) {
+      const int k = r.k;
+      std::vector<int32_t> key(m0ids.begin() + r.ids, m0ids.begin() + r.ids + k);
+      key.push_back(k);
+      key.push_back(k);
+      int32_t gid;
+      auto f = gmap.find(key);
+      if (f != gmap.end()) {
+        gid = f->second;
+      } else {
+        gid = (int32_t)h_gku.size();
+        gmap.emplace(key, gid);
+        const int L = N - k + 1;
+        h_gku.push_back(k | (k << 8));
+        h_goff.push_back((int64_t)h_gtab.size());
+        h_gtab.resize(h_gtab.size() + L + (size_t)k * L + k, 0.0);
+        long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - k);
+        for (int q = 0; q < k; ++q) ids[q] = key[q];
+        for (int q = 0; q < k; ++q) h_items.push_back(((long long)gid << 8) | q);
+        gm0.push_back(0.0L);
+        granges.emplace_back();
+      }
+      if (wuni[k]) gm0[gid] += (long double)wconst[k] * (long double)r.cnt;
+      else if (r.w1 > r.w0) granges[gid].push_back({r.w0, r.w1});
+    }
+    h_gm0w.resize(h_gku.size());
+    h_gcoff.resize(h_gku.size() + 1);
+    constexpr int64_t kChunk = 4096;  // weights per m0sum_kernel chunk (a warp each)
+    for (size_t g = 0; g < h_gku.size(); ++g) {
+      h_gm0w[g] = (double)gm0[g];
+      h_gcoff[g] = (int64_t)h_m0chunk.size();
+      for (const auto& rg : granges[g])
+        for (int64_t a = rg.first; a < rg.second; a += kChunk)
+          h_m0chunk.push_back(((long long)a << 13) | (long long)std::min<int64_t>(kChunk, rg.second - a));
+      if (h_gm0w[g] != 0.0 || h_gcoff[g] < (int64_t)h_m0chunk.size()) ++p->m0_groups;
+    }
+    h_gcoff[h_gku.size()] = (int64_t)h_m0chunk.size();
+    p->m0_chunks = (int64_t)h_m0chunk.size();
+    // group_kernel items ordered by the prefix member's vertex, so a warp's M = 0
+    // deposits to one vertex (the hottest are in most groups) aggregate into one red
+    {
+      std::vector<std::pair<long long, long long>> keyed(h_items.size());
+      for (size_t t = 0; t < h_items.size(); ++t) {
+        const int64_t g = h_items[t] >> 8;
+        const int i = (int)(h_items[t] & 255);
+        const int k = h_gku[g] & 255, u = h_gku[g] >> 8, L = N - k + 1;
+        const long long v = reinterpret_cast<const long long*>(h_gtab.data() + h_goff[g] + L + (size_t)u * L)[i];
+        keyed[t] = {v, h_items[t]};
+      }
+      std::stable_sort(keyed.begin(), keyed.end());
+      for (size_t t = 0; t < h_items.size(); ++t) h_items[t] = keyed[t].second;
     }
     p->prefix_groups = (int64_t)h_gku.size();
     // the group kernel is instantiated up to the largest L of the plan's groups (kernels.cu)
@@ -821,8 +953,11 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   const size_t b_tu = align(h_hdr.size() * 8 + 8), b_tg = 0;
   const size_t b_gku = align(h_gku.size() * 4 + 4), b_goff = align(h_goff.size() * 8 + 8),
                b_gtab = align(h_gtab.size() * 8 + 8), b_items = align(h_items.size() * 8 + 8);
+  const size_t b_gm0w = align(h_gm0w.size() * 8 + 8), b_gcoff = align(h_gcoff.size() * 8 + 8),
+               b_m0chunk = align(h_m0chunk.size() * 8 + 8), b_w0 = align(h_w0.size() * 8 + 8),
+               b_m0sum = align(h_m0chunk.size() * 8 + 8);
   p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg + b_gku + b_goff + b_gtab +
-              b_items;
+              b_items + b_gm0w + b_gcoff + b_m0chunk + b_w0 + b_m0sum;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -841,6 +976,12 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   int64_t* d_goff = (int64_t*)(gbase + b_gku);
   double* d_gtab = (double*)(gbase + b_gku + b_goff);
   long long* d_items = (long long*)(gbase + b_gku + b_goff + b_gtab);
+  char* mbase = gbase + b_gku + b_goff + b_gtab + b_items;
+  double* d_gm0w = (double*)mbase;
+  int64_t* d_gcoff = (int64_t*)(mbase + b_gm0w);
+  long long* d_m0chunk = (long long*)(mbase + b_gm0w + b_gcoff);
+  double* d_w0 = (double*)(mbase + b_gm0w + b_gcoff + b_m0chunk);
+  p->d_m0sum = (double*)(mbase + b_gm0w + b_gcoff + b_m0chunk + b_w0);
   p->gs = gs;
   if (ids_total && idb == 4) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ids_total && idb == 2) {
@@ -856,6 +997,15 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (ce == cudaSuccess && !h_gtab.empty()) ce = cudaMemcpy(d_gtab, h_gtab.data(), h_gtab.size() * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_items.empty())
     ce = cudaMemcpy(d_items, h_items.data(), h_items.size() * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_gm0w.empty()) ce = cudaMemcpy(d_gm0w, h_gm0w.data(), h_gm0w.size() * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_gcoff.empty()) ce = cudaMemcpy(d_gcoff, h_gcoff.data(), h_gcoff.size() * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_m0chunk.empty())
+    ce = cudaMemcpy(d_m0chunk, h_m0chunk.data(), h_m0chunk.size() * 8, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !h_w0.empty()) ce = cudaMemcpy(d_w0, h_w0.data(), h_w0.size() * 8, cudaMemcpyHostToDevice);
+  p->d_gm0w = h_gm0w.empty() ? nullptr : d_gm0w;
+  p->d_gcoff = h_gcoff.empty() ? nullptr : d_gcoff;
+  p->d_m0chunk = d_m0chunk;
+  p->d_w0 = d_w0;
   p->d_items = d_items;
   p->nitems = (int64_t)h_items.size();
   kp.tile_hdr = h_hdr.empty() ? nullptr : d_hdr;
@@ -935,6 +1085,9 @@ extern "C" sttsv_status_t sttsv_plan_info(sttsv_plan_t p, sttsv_plan_info_t* inf
   info->prefix_groups = p->prefix_groups;
   info->prefix_incidences = p->prefix_inc;
   info->num_tiles = p->kp.num_tiles;
+  info->m0_edges = p->m0_edges;
+  info->m0_groups = p->m0_groups;
+  info->m0_chunks = p->m0_chunks;
   return STTSV_OK;
 }
 
@@ -944,6 +1097,7 @@ extern "C" int sttsv_apply_launches(sttsv_plan_t p) {
   if (p->n_active > 0) l += 2;          // gather + expand
   if (p->kp.num_tiles > 0) l += 1;      // edge kernel
   if (p->kp.gtab) l += 1;               // shared-prefix group table
+  if (p->m0_chunks > 0) l += 1;         // M = 0 weight sums
   if (p->det) l += 2;                   // deterministic chunk + vertex sums
   return l;
 }
@@ -988,7 +1142,8 @@ static sttsv_status_t check_async(sttsv_plan_s* p) {
 static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed = false) {
   if (p->n_active == 0) return STTSV_OK;
   if (!p->det && !zeroed) CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
-  if (p->kp.num_tiles > 0) {
+  const bool groups = p->kp.gtab != nullptr;
+  if (p->kp.num_tiles > 0 || groups) {
     std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
     if (p->profiling) {
       if (p->events_used == p->events.size()) {
@@ -1000,12 +1155,17 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
       ev = &p->events[p->events_used++];
       CUDA_TRY(cudaEventRecord(ev->first, s), "cudaEventRecord");
     }
-    const bool groups = p->kp.gtab != nullptr;
-    if (groups)  // per-apply shared-prefix group table (prefix.cuh)
+    // the M = 0 runs' weight sums (x-independent; prefix.cuh), then the per-apply
+    // shared-prefix group table with the M = 0 deposits (prefix.cuh)
+    if (p->m0_chunks > 0)
+      CUDA_TRY(launch_m0sum(p->d_w0, p->d_m0chunk, p->m0_chunks, p->d_m0sum, s), "m0sum launch");
+    if (groups)
       CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->d_items, p->nitems, p->group_lmax,
-                             p->kp.gtab, const_cast<double*>(p->kp.gtab), s), "group kernel launch");
-    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0, zeroed || groups),
-             "edge kernel launch");
+                             p->kp.gtab, const_cast<double*>(p->kp.gtab), p->d_gm0w, p->d_gcoff, p->d_m0sum,
+                             p->d_ya, s), "group kernel launch");
+    if (p->kp.num_tiles > 0)
+      CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0,
+                                  groups || (zeroed && p->m0_chunks == 0)), "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }
   if (p->det)  // fixed-order sums of the vertex-major buffer (every active vertex written)
@@ -1239,7 +1399,7 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
                            p->gs, p->ent.table_norm, na, s), "gather launch");
   if (na > 0) {
     CUDA_TRY(cudaMemsetAsync(p->b_ya, 0, (size_t)nvec * na * sizeof(double), s), "memset y_a");
-    if (p->kp.num_tiles > 0) {
+    if (p->kp.num_tiles > 0 || p->kp.gtab) {
       EdgeKernelParams kp = p->kp;
       kp.nvec = nvec;
       kp.xa = p->b_xa;
@@ -1251,16 +1411,20 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       // shared-prefix memo: one group table per vector (prefix.cuh)
       const bool groups = p->kp.gtab != nullptr;
       if (groups) {
+        if (p->m0_chunks > 0)
+          CUDA_TRY(launch_m0sum(p->d_w0, p->d_m0chunk, p->m0_chunks, p->d_m0sum, s), "m0sum launch");
         for (int v = 0; v < nvec; ++v)
           CUDA_TRY(launch_groups(p->b_xg + (size_t)v * na * p->gs, p->gs, p->N, p->d_gku, p->d_goff, p->d_items,
-                                 p->nitems, p->group_lmax, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles, s),
+                                 p->nitems, p->group_lmax, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles,
+                                 p->d_gm0w, p->d_gcoff, p->d_m0sum, p->b_ya + (size_t)v * na, s),
                    "group kernel launch");
         kp.gtab = p->b_gtab;
         kp.gtab_vstride = p->gtab_doubles;
       }
       kp.group_wait = groups;
-      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0), groups),
-               "edge kernel launch");
+      if (p->kp.num_tiles > 0)
+        CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0), groups),
+                 "edge kernel launch");
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,
                                              p->b_ya, na, s), "deterministic reduce launch");
     }

@@ -47,7 +47,8 @@ class PlanInfo(ctypes.Structure):
                 ("hot_shared", ctypes.c_int32), ("kernel_grid", ctypes.c_int32), ("kernel_block", ctypes.c_int32),
                 ("id_bytes", ctypes.c_int32), ("allreduces", ctypes.c_int64), ("fma_executed", ctypes.c_double),
                 ("prefix_tiles", ctypes.c_int64), ("prefix_groups", ctypes.c_int64),
-                ("prefix_incidences", ctypes.c_int64), ("num_tiles", ctypes.c_int64)]
+                ("prefix_incidences", ctypes.c_int64), ("num_tiles", ctypes.c_int64),
+                ("m0_edges", ctypes.c_int64), ("m0_groups", ctypes.c_int64), ("m0_chunks", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "edges_per_size"}

@@ -576,3 +576,66 @@ def test_prefix_memo(S, torch_cuda, N, kmax):
     assert rel(y2, oracle.sttsv(hg, x=x2)) < TOL
     plan.close()
     nplan.close()
+
+
+# ------------------------------------------ M = 0 runs (prefix.cuh: one repeated vertex set)
+@pytest.mark.parametrize("N,uniform", [(5, True), (5, False), (8, True), (12, False), (25, True), (25, False)])
+def test_m0_runs(S, torch_cuda, N, uniform):
+    """Long runs of one repeated vertex set leave the tile stream (plan info m0_edges); the
+    group kernel deposits C_i[0] times the run's summed w' (a plan-time count for uniform
+    weights, per-apply chunk sums of the stored weights otherwise).  Against the oracle on
+    the same hypergraph, through apply, the batched apply (both strategies) and 3 power steps."""
+    torch = torch_cuda
+    rng = np.random.default_rng(700 + N + 1000 * uniform)
+    n = 300
+    edges = []
+    kmax = min(N, 8) if N <= 12 else 4  # (the oracle's kappa enumeration grows fast with N and k)
+    for _ in range(10):
+        k = int(rng.integers(1, kmax + 1))
+        s = sorted(rng.choice(n, size=k, replace=False).tolist())
+        edges += [s] * int(rng.integers(300, 9000))      # runs of one set (many whole warp blocks)
+        for _ in range(int(rng.integers(0, 200))):        # and distinct edges around them
+            k2 = int(rng.integers(1, kmax + 1))
+            edges.append(sorted(rng.choice(n, size=k2, replace=False).tolist()))
+    rng.shuffle(edges)
+    w = np.ones(len(edges)) if uniform else rng.uniform(0.1, 2.0, len(edges))
+    hg = to_hg(n, N, edges, w, rng.uniform(0.05, 1.0, n))
+    plan = S.Plan.from_hypergraph(hg)
+    info = plan.info()
+    assert info["m0_edges"] > 0 and info["m0_groups"] > 0, info
+    assert (info["m0_chunks"] == 0) == uniform, info
+    assert info["stored_edges"] == hg.m
+    x = torch.from_numpy(hg.x).cuda()
+    ref = oracle.sttsv(hg)
+    assert rel(plan.apply(x).cpu().numpy(), ref) < TOL
+    x2 = rng.uniform(0.05, 1.0, n)
+    assert rel(plan.apply(torch.from_numpy(x2).cuda()).cpu().numpy(), oracle.sttsv(hg, x=x2)) < TOL
+    X = torch.from_numpy(np.stack([hg.x, x2])).cuda().contiguous()
+    for fused in (False, True):
+        bp = S.Plan.from_hypergraph(hg, flags=S.STTSV_BATCH_FUSED) if fused else plan
+        Y = bp.apply_batch(X).cpu().numpy()
+        assert rel(Y[0], ref) < TOL and rel(Y[1], oracle.sttsv(hg, x=x2)) < TOL
+        if fused:
+            bp.close()
+    if N >= 2:
+        x0 = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+        xo, zo = oracle.power_iteration(hg, 3)
+        xg, zg = plan.power_iterate(x0, 3)
+        assert rel(xg.cpu().numpy(), xo) < TOL and rel(zg.cpu().numpy(), zo) < TOL
+    plan.close()
+
+
+def test_m0_only_plan(S, torch_cuda):
+    """Every edge the same vertex set: no tile stream at all (num_tiles 0), only the group kernel."""
+    torch = torch_cuda
+    edges = [[3, 7, 11]] * 5000 + [[2]] * 3000
+    rng = np.random.default_rng(5)
+    for uniform in (True, False):
+        w = np.ones(len(edges)) if uniform else rng.uniform(0.1, 2.0, len(edges))
+        hg = to_hg(20, 6, edges, w, rng.uniform(0.05, 1.0, 20))
+        plan = S.Plan.from_hypergraph(hg)
+        info = plan.info()
+        assert info["num_tiles"] == 0 and info["m0_edges"] == len(edges), info
+        y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
+        assert rel(y, oracle.sttsv(hg)) < TOL
+        plan.close()

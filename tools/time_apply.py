@@ -51,8 +51,22 @@ if hasattr(lib, "sttsv_debug_wait"):
     lib.sttsv_debug_kcycles(kb, 1)
     tot = sum(kb[2 * k] for k in range(33)) or 1
     info = plan.info()
+    if os.environ.get("WAITPROF_CLASSES"):
+        for c in range(33):
+            if kb[2 * c + 1]:
+                lab = "M=0" if c == 0 else ("M=%d" % c if c < 20 else "full k=%d" % (c - 20))
+                print("  %-10s warp-blocks=%9d cycles share %5.1f%%  cyc/block %.0f" % (
+                    lab, kb[2 * c + 1], 100.0 * kb[2 * c] / tot, kb[2 * c] / kb[2 * c + 1]))
+        cb = (ctypes.c_ulonglong * 3072)()
+        lib.sttsv_debug_cta(cb, 1)
+        g = info["kernel_grid"]
+        st = [cb[3 * i] for i in range(g)]; en = [cb[3 * i + 1] for i in range(g)]; nt = [cb[3 * i + 2] for i in range(g)]
+        t0 = min(st)
+        ends = sorted((e - t0) / 1e3 for e in en)
+        print("  CTA start spread %.1f us; end (us after first start): min %.1f median %.1f max %.1f; tiles/CTA min %d max %d" % (
+            (max(st) - t0) / 1e3, ends[0], ends[len(ends) // 2], ends[-1], min(nt), max(nt)))
     for k in range(33):
-        if kb[2 * k + 1]:
+        if kb[2 * k + 1] and not os.environ.get("WAITPROF_CLASSES"):
             print("  k=%2d warp-tiles=%8d cycles share %5.1f%%  edges share %5.1f%%  cyc/warp-tile %.0f" % (
                 k, kb[2 * k + 1], 100.0 * kb[2 * k] / tot, 100.0 * info["edges_per_size"][k] / max(info["num_edges"], 1),
                 kb[2 * k] / kb[2 * k + 1]))
