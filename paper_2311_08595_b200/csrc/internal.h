@@ -23,7 +23,7 @@ struct BucketDesc {
   double wc;           // the common w' of a uniform-weight bucket
 };
 
-constexpr int kMaxBuckets = STTSV_MAX_RANK;
+constexpr int kMaxBuckets = 2 * STTSV_MAX_RANK;  // per size k: the input edges and (plan.cpp) the M = 0 runs' representatives
 
 // Row stride (doubles) of the per-apply series table x_g (dp.cuh): coefficients
 // j = 0..N-2 are used (L - 1 <= N - 2 for k >= 2; the singleton needs j = N - 2),
@@ -131,14 +131,16 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 // items[t] = (group << 8) | i, one per prefix member of every group; gtab_in: the
 // plan's table (its prefix ids); gtab_out receives A, C (and the ids when it is a
 // batch vector's copy)
-// M = 0 runs: item (g, i) also deposits C_i[0] * t0 into ya[id], t0 = gm0w[g] + the
-// chunk sums m0sum[gcoff[g] .. gcoff[g+1]) (gm0w == nullptr: no M = 0 groups)
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
                           const long long* items, int64_t nitems, int lmax, const double* gtab_in,
-                          double* gtab_out, const double* gm0w, const int64_t* gcoff, const double* m0sum,
-                          double* ya, cudaStream_t s);
-// m0sum[c] = sum of w0 over chunk c (chunk[c] = (first << 13) | length), one warp per chunk
-cudaError_t launch_m0sum(const double* w0, const long long* chunk, int64_t nchunks, double* m0sum, cudaStream_t s);
+                          double* gtab_out, cudaStream_t s);
+// M = 0 runs (plan.cpp): each representative's weight = the sum of its run's stored
+// weights w0, one warp job per (x, y) pair of job[] (kernels.cu m0sum_kernel): whole
+// runs, chunks of split runs (rc0 / wpos per split run, part / cnt: per-job partial sums
+// and per-run counters, zero at rest) and packs of short runs (pentry).
+cudaError_t launch_m0sum(const double* w0, const long long* job, int64_t njobs, const long long* pentry,
+                         const int64_t* rc0, const int64_t* wpos, double* part, unsigned int* cnt, double* w,
+                         cudaStream_t s);
 cudaError_t launch_expand(const double* ya, const int32_t* act, double* y, int64_t n_active, cudaStream_t s);
 constexpr int kNormalizeScratch = 296;  // blocks of the reduction kernels (scratch: 2x doubles + 2)
 cudaError_t launch_normalize(const double* z, double* x, double* xg, int gs, int norm, double* partial,

@@ -63,8 +63,8 @@ __global__ void series_kernel(const double* __restrict__ xa, double* __restrict_
 // kernel that follows is a programmatic dependent launch (its consumers wait for
 // this grid before reading the table).
 template <int L>
-__device__ __forceinline__ double group_item(const double* __restrict__ xg, int gs, const long long* ids, int U, int i,
-                                             double* T, long long* ids_out) {
+__device__ __forceinline__ void group_item(const double* __restrict__ xg, int gs, const long long* ids, int U, int i,
+                                           double* T, long long* ids_out) {
   constexpr int D = L - 1;
   double ah[L], ai[L];
   double X = 1.0, Xi = 1.0;
@@ -100,100 +100,127 @@ __device__ __forceinline__ double group_item(const double* __restrict__ xg, int 
   double* C = T + L + i * L;
 #pragma unroll
   for (int j = 0; j <= D; ++j) C[j] = Xi * ai[D - j] + (j <= D - 1 ? X * ah[D - 1 - j] : 0.0);
-  return Xi * ai[D] + (D >= 1 ? X * ah[D >= 1 ? D - 1 : 0] : 0.0);  // C_i[0]
 }
 
 template <int L, int LMAX>
-__device__ __forceinline__ double group_item_dispatch(int L_rt, const double* xg, int gs, const long long* ids,
-                                                      int U, int i, double* T, long long* ids_out) {
+__device__ __forceinline__ void group_item_dispatch(int L_rt, const double* xg, int gs, const long long* ids, int U,
+                                                    int i, double* T, long long* ids_out) {
   if constexpr (L <= LMAX) {
-    if (L_rt == L) return group_item<L>(xg, gs, ids, U, i, T, ids_out);
-    return group_item_dispatch<L + 1, LMAX>(L_rt, xg, gs, ids, U, i, T, ids_out);
-  }
-  return 0.0;
-}
-
-// Warp-wide deposit: lanes with v >= 0 add d to ya[v]; runs of equal adjacent v
-// (the items are ordered by vertex) are summed first and deposited with one red.
-__device__ __forceinline__ void warp_deposit(int64_t v, double d, double* ya) {
-  const int lane = threadIdx.x & 31;
-  const int64_t vn = __shfl_down_sync(0xffffffffu, v, 1);
-  int f = (lane == 31) || (vn != v);  // last lane of its run
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {  // segmented suffix sum: a lane ends with its run's sum from itself on
-    const double dn = __shfl_down_sync(0xffffffffu, d, o);
-    const int fn = __shfl_down_sync(0xffffffffu, f, o);
-    if (!f && lane + o < 32) {
-      d += dn;
-      f = fn;
+    if (L_rt == L) {
+      group_item<L>(xg, gs, ids, U, i, T, ids_out);
+      return;
     }
+    group_item_dispatch<L + 1, LMAX>(L_rt, xg, gs, ids, U, i, T, ids_out);
   }
-  const int64_t vp = __shfl_up_sync(0xffffffffu, v, 1);
-  if ((lane == 0 || vp != v) && v >= 0)
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(ya + v), "d"(d) : "memory");
 }
 
-// Instantiated up to the plan's largest L (launch_groups): a kernel's register count is
-// the maximum over the L it instantiates, so plans with short series get full occupancy.
 template <int LMIN, int LMAX>
 __global__ void __launch_bounds__(128) group_kernel(const double* __restrict__ xg, int gs, int N,
                                                     const int32_t* __restrict__ gku, const int64_t* __restrict__ goff,
                                                     const long long* __restrict__ items, int64_t nitems,
-                                                    const double* gtab_in, double* gtab,
-                                                    const double* __restrict__ gm0w,
-                                                    const int64_t* __restrict__ gcoff,
-                                                    const double* __restrict__ m0sum, double* ya) {
+                                                    const double* gtab_in, double* gtab) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int lane = threadIdx.x & 31;
-  // warp-uniform loop (the M = 0 deposit is warp-wide)
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < nitems;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nitems;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t v = -1;
-    double d = 0.0;
-    if (t < nitems) {
-      const long long it = items[t];
-      const int64_t g = it >> 8;
-      const int i = (int)(it & 255);
-      const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1;
-      const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
-      double* T = gtab + goff[g];
-      long long* ids_out = gtab_in != gtab ? reinterpret_cast<long long*>(T + L + U * L) : nullptr;
-      const double c0 = group_item_dispatch<LMIN, LMAX>(L, xg, gs, ids, U, i, T, ids_out);
-      if (gm0w) {
-        // M = 0 runs of this group (U = k): member i gets C_i[0] * (sum of their w')
-        double t0 = gm0w[g];
-        for (int64_t c = gcoff[g]; c < gcoff[g + 1]; ++c) t0 += m0sum[c];
-        if (t0 != 0.0) {
-          v = ids[i];
-          d = c0 * t0;
-        }
-      }
-    }
-    if (gm0w) warp_deposit(v, d, ya);
+    const long long it = items[t];
+    const int64_t g = it >> 8;
+    const int i = (int)(it & 255);
+    const int k = gku[g] & 255, U = gku[g] >> 8, L = N - k + 1;
+    const long long* ids = reinterpret_cast<const long long*>(gtab_in + goff[g] + L + U * L);
+    double* T = gtab + goff[g];
+    long long* ids_out = gtab_in != gtab ? reinterpret_cast<long long*>(T + L + U * L) : nullptr;
+    group_item_dispatch<LMIN, LMAX>(L, xg, gs, ids, U, i, T, ids_out);
   }
 }
 
-// Sum of each chunk of the M = 0 weight column (prefix.cuh), one warp per chunk:
-// the weights are read once per apply (8 independent loads in flight per lane).
-__global__ void __launch_bounds__(256) m0sum_kernel(const double* __restrict__ w0, const long long* __restrict__ chunk,
-                                                    int64_t nchunks, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < nchunks;
-       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const long long ch = chunk[c];
-    const double* p = w0 + (ch >> 13);
-    const int len = (int)(ch & 8191);
-    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int j = lane;
-    for (; j + 7 * 32 < len; j += 8 * 32) {
+// Weights of the M = 0 runs' representative edges (plan.cpp): representative r
+// stands for a run of one repeated vertex set and takes w' summed over the run's
+// stored weights w0[...] (read every apply).  One warp per job; a job is one
+// 16-byte record, so its loads of w0 issue right after it (no dependent metadata):
+//   x = (a << 24) | n, y >= 0      a whole run w0[a .. a+n) (n <= 2048): w[y] = its sum
+//   x = (a << 24) | n, y < 0       a chunk of split run r = -1 - y: the run's chunks (jobs
+//                                  rc0[2r] .. rc0[2r+1]) store partial sums; the last to
+//                                  finish (a per-run counter, reset by it) adds them, the
+//                                  whole warp in a fixed order, into w[wpos[r]]
+//   x = 2^62 | (a << 24) | n       a pack of neighbouring short runs in w0[a .. a+n)
+//                                  (n <= 256), y = (first entry << 9) | runs; entry
+//                                  (wpos << 18) | (offset << 9) | length per run
+// The loads of a whole run / chunk keep 8 independent loads in flight per lane.
+constexpr int kM0Block = 256, kM0Pack = 256;
+__global__ void __launch_bounds__(kM0Block) m0sum_kernel(const double* __restrict__ w0,
+                                                         const longlong2* __restrict__ job, int64_t njobs,
+                                                         const long long* __restrict__ pentry,
+                                                         const int64_t* __restrict__ rc0,
+                                                         const int64_t* __restrict__ wpos, double* __restrict__ part,
+                                                         unsigned int* __restrict__ cnt, double* __restrict__ w) {
+  __shared__ double sbuf[kM0Block / 32][kM0Pack];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < njobs; c += nwarps) {
+    const longlong2 jb = job[c];
+    const long long x = jb.x, y = jb.y;
+    const double* p = w0 + ((x >> 24) & ((1ll << 38) - 1));
+    const int len = (int)(x & 0xffffff);
+    if (!((x >> 62) & 1)) {
+      double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int j = lane;
+      for (; j + 7 * 32 < len; j += 8 * 32) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) s[q] += __ldcs(p + j + q * 32);
+        for (int q = 0; q < 8; ++q) s[q] += __ldcs(p + j + q * 32);
+      }
+      for (; j < len; j += 32) s[0] += __ldcs(p + j);
+      double r = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+      if (y >= 0) {
+        if (lane == 0) w[y] = r;
+        continue;
+      }
+      const int64_t run = -1 - y;
+      unsigned last = 0u;
+      if (lane == 0) {
+        part[c] = r;
+        __threadfence();
+        last = atomicAdd(cnt + run, 1u) == (unsigned)(rc0[2 * run + 1] - rc0[2 * run] - 1) ? 1u : 0u;
+      }
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        __threadfence();
+        const int64_t a = rc0[2 * run], b = rc0[2 * run + 1];
+        double t0 = 0.0, t1 = 0.0;
+        int64_t q = a + lane;
+        for (; q + 32 < b; q += 64) {
+          t0 += __ldcg(part + q);
+          t1 += __ldcg(part + q + 32);
+        }
+        if (q < b) t0 += __ldcg(part + q);
+        double tot = t0 + t1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0) {
+          w[wpos[run]] = tot;
+          cnt[run] = 0u;
+        }
+      }
+    } else {
+      const int64_t e0 = y >> 9;
+      const int nr = (int)(y & 511);
+      const long long ent = lane < nr ? pentry[e0 + lane] : 0ll;  // runs beyond 32: loaded below
+      double* sb = sbuf[wib];
+#pragma unroll
+      for (int j = 0; j < kM0Pack / 32; ++j)
+        if (lane + 32 * j < len) sb[lane + 32 * j] = __ldcs(p + lane + 32 * j);
+      __syncwarp();
+      for (int i = 0; i < nr; ++i) {  // warp-wide sum of each run
+        const long long e = i < 32 ? __shfl_sync(0xffffffffu, ent, i) : pentry[e0 + i];
+        const int off = (int)((e >> 9) & 511), n = (int)(e & 511);
+        double r = 0.0;
+        for (int j = lane; j < n; j += 32) r += sb[off + j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (lane == 0) w[e >> 18] = r;
+      }
+      __syncwarp();
     }
-    for (; j < len; j += 32) s[0] += __ldcs(p + j);
-    double r = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if (lane == 0) out[c] = r;
   }
 }
 
@@ -460,24 +487,26 @@ cudaError_t launch_series(const double* xa, double* xg, int gs, int norm, int64_
 
 cudaError_t launch_groups(const double* xg, int gs, int N, const int32_t* gku, const int64_t* goff,
                           const long long* items, int64_t nitems, int lmax, const double* gtab_in,
-                          double* gtab_out, const double* gm0w, const int64_t* gcoff, const double* m0sum,
-                          double* ya, cudaStream_t s) {
+                          double* gtab_out, cudaStream_t s) {
   // one launch, instantiated up to the plan's largest L (a kernel's register count is
   // the maximum over the L it instantiates: 72 / 134 / 254 for L <= 8 / 16 / 32)
   if (nitems <= 0) return cudaSuccess;
   const int g = grid_for(nitems, 128, 8192);
   if (lmax <= 8)
-    group_kernel<1, 8><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out, gm0w, gcoff, m0sum, ya);
+    group_kernel<1, 8><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
   else if (lmax <= 16)
-    group_kernel<1, 16><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out, gm0w, gcoff, m0sum, ya);
+    group_kernel<1, 16><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
   else
-    group_kernel<1, STTSV_MAX_RANK><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out, gm0w, gcoff, m0sum, ya);
+    group_kernel<1, STTSV_MAX_RANK><<<g, 128, 0, s>>>(xg, gs, N, gku, goff, items, nitems, gtab_in, gtab_out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_m0sum(const double* w0, const long long* chunk, int64_t nchunks, double* m0sum, cudaStream_t s) {
-  if (nchunks <= 0) return cudaSuccess;
-  m0sum_kernel<<<grid_for(nchunks * 32, 256, 148 * 16), 256, 0, s>>>(w0, chunk, nchunks, m0sum);
+cudaError_t launch_m0sum(const double* w0, const long long* job, int64_t njobs, const long long* pentry,
+                         const int64_t* rc0, const int64_t* wpos, double* part, unsigned int* cnt, double* w,
+                         cudaStream_t s) {
+  if (njobs <= 0) return cudaSuccess;
+  m0sum_kernel<<<grid_for(32 * njobs, kM0Block, 148 * 8), kM0Block, 0, s>>>(
+      w0, reinterpret_cast<const longlong2*>(job), njobs, pentry, rc0, wpos, part, cnt, w);
   return cudaGetLastError();
 }
 

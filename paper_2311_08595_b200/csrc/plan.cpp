@@ -275,15 +275,18 @@ struct sttsv_plan_s {
   int group_lmax = 0;                    // largest L among the prefix groups
   int64_t nitems = 0;
   int64_t prefix_tiles = 0, prefix_groups = 0, prefix_inc = 0;
-  // M = 0 runs (prefix.cuh): edges whose warp block is one vertex set leave the tile
-  // stream; group_kernel deposits C_i[0] * t0 with t0 = m0w[g] (uniform-weight
-  // buckets: w' x edges) + the group's chunk sums of the stored weights (m0sum_kernel)
+  // M = 0 runs (plan_create): edges whose warp block is one vertex set leave the tile
+  // stream; each run is one representative edge whose weight is the run's summed w'
+  // (plan-time for uniform-weight buckets, m0sum_kernel every apply otherwise)
   int64_t m0_edges = 0, m0_groups = 0, m0_chunks = 0;
-  const double* d_gm0w = nullptr;     // per group: the uniform-weight part of t0
-  const int64_t* d_gcoff = nullptr;   // per group: its chunks gcoff[g] .. gcoff[g+1]
-  const long long* d_m0chunk = nullptr;  // per chunk: (first weight << 13) | length
-  const double* d_w0 = nullptr;       // the M = 0 edges' weights of non-uniform buckets
-  double* d_m0sum = nullptr;          // per chunk: its weight sum (per apply)
+  const long long* d_m0job = nullptr;    // m0sum_kernel jobs (x, y) pairs (kernels.cu)
+  const long long* d_pentry = nullptr;   // per short run of a pack: (wpos << 18) | (offset << 9) | length
+  const int64_t* d_rc0 = nullptr;        // per split run: its chunk jobs rc0[2r] .. rc0[2r+1]
+  const int64_t* d_wpos = nullptr;       // per split run: its representative's weight slot
+  const double* d_w0 = nullptr;          // the runs' stored weights
+  double* d_m0part = nullptr;            // per chunk: partial sum (runs of several chunks)
+  unsigned int* d_m0cnt = nullptr;       // per run: chunks done (reset by the last)
+  double* d_wpool = nullptr;             // the plan's weight pool (the representatives' slots)
   // edge-kernel timing (sttsv_plan_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
@@ -453,7 +456,11 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   p->ent = edge_entry(N, na <= 65536 && !getenv("STTSV_ID32"));
   const int tile = p->ent.tile;
   const int idb = p->ent.id_bytes;  // 2: 16-bit member ids in the edge stream
-  std::vector<int64_t> lo(N + 1), mk(N + 1, 0), stride(N + 1, 0);
+  // bucket index bi: 1..N the input edges of size bi, N + k the representatives of the
+  // size-k M = 0 runs (below)
+  const int NB = 2 * N;
+  auto ksz = [N](int bi) { return bi <= N ? bi : bi - N; };
+  std::vector<int64_t> lo(N + 1), mk(NB + 1, 0), stride(NB + 1, 0);
   for (int k = 1; k <= N; ++k) {
     lo[k] = bucket_lo(count[k], world, rank);
     mk[k] = bucket_lo(count[k], world, rank + 1) - lo[k];
@@ -463,7 +470,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     p->local_inc += mk[k] * k;
   }
   // pools: ids [sum_k k*stride_k] int32, w [sum_k stride_k] f64
-  std::vector<int64_t> ids_off(N + 1, 0), w_off(N + 1, 0);
+  std::vector<int64_t> ids_off(NB + 1, 0), w_off(NB + 1, 0);
   int64_t ids_total = 0, w_total = 0;
   for (int k = 1; k <= N; ++k) {
     ids_off[k] = ids_total;
@@ -483,7 +490,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     rows_total += (int64_t)k * mk[k];
   }
   std::vector<int32_t> rows((size_t)rows_total);
-  std::vector<int64_t> stored(N + 1, 0);  // edges stored per bucket (after optional merging)
+  std::vector<int64_t> stored(NB + 1, 0);  // edges stored per bucket (after optional merging)
   std::vector<double> wrow((size_t)w_total);
 #pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < m; ++e) {
@@ -503,10 +510,10 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   }
   // shared-prefix memo: per warp block (the NCW blocks of 32*epl consecutive sorted
   // edges of a tile, one per consumer warp) the shared prefix length U
-  std::vector<std::vector<uint8_t>> tile_u(N + 1);
+  std::vector<std::vector<uint8_t>> tile_u(NB + 1);
   const int nblk = p->ent.consumers / 32, wblk = tile / nblk;
-  std::vector<int> wuni(N + 1, 0);
-  std::vector<double> wconst(N + 1, 0.0);
+  std::vector<int> wuni(NB + 1, 0);
+  std::vector<double> wconst(NB + 1, 0.0);
   // The memo pays once the stream is long enough to amortise its group-table kernel and
   // per-block control work: measured on B200, mid (1e6 edges) runs faster without it and
   // high-rank (5e6) faster with it; below kMemoMinEdges a plan uses the plain per-edge path
@@ -515,6 +522,19 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (const char* env = getenv("STTSV_MEMO_MIN_EDGES")) memo_min = atoll(env);
   const bool memo = p->ent.prefix_mmax > 0 && !(flags & (STTSV_DETERMINISTIC | STTSV_NO_PREFIX_MEMO)) &&
                     !getenv("STTSV_NO_PREFIX") && p->local_edges >= memo_min;
+  // shared-prefix memo: per warp block of wblk consecutive sorted edges, the length U of
+  // the member prefix all its edges share (0: none usable, the block runs the full DP)
+  auto block_u = [&](int k, const int32_t* col, int64_t st, std::vector<uint8_t>& tu) {
+    const int L = N - k + 1;
+    for (int64_t bl = 0; bl < (int64_t)tu.size(); ++bl) {
+      const int64_t j0 = bl * wblk, j1 = j0 + wblk - 1;
+      int u = 0;
+      while (u < k && col[(int64_t)u * st + j0] == col[(int64_t)u * st + j1]) ++u;
+      const int M = k - u;
+      const bool ok = u >= 1 && (M == 0 || (M <= p->ent.prefix_mmax && L <= p->ent.prefix_lmax));
+      tu[bl] = (uint8_t)(ok ? u : 0);
+    }
+  };
   struct M0Run {
     int k;
     int64_t ids;     // offset of its vertex set in m0ids
@@ -585,21 +605,15 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     const int64_t ntl = padded / tile;
     tile_u[k].assign(ntl * nblk, 0);
     if (memo) {
-      const int L = N - k + 1;
-      for (int64_t bl = 0; bl < ntl * nblk; ++bl) {  // warp blocks of wblk consecutive sorted edges
-        const int64_t j0 = bl * wblk, j1 = j0 + wblk - 1;
-        int u = 0;
-        while (u < k && col[(int64_t)u * st + j0] == col[(int64_t)u * st + j1]) ++u;
-        const int M = k - u;
-        const bool ok = u >= 1 && (M == 0 || (M <= p->ent.prefix_mmax && L <= p->ent.prefix_lmax));
-        tile_u[k][bl] = (uint8_t)(ok ? u : 0);
-      }
+      block_u(k, col, st, tile_u[k]);
       // M = 0 blocks (U = k: every edge of the block is the same vertex set) leave the
-      // tile stream.  Their contribution is w' summed over the block times the group's
-      // C_i[0] (prefix.cuh); consecutive blocks of one set form one run.  Uniform-weight
-      // buckets keep the run's edge count (t0 = w' x count); otherwise the run's weights
-      // move to the M = 0 weight column that m0sum_kernel sums every apply.  The kept
-      // blocks are compacted in order and the bucket is re-padded to whole tiles.
+      // tile stream.  B is linear in w, so a run of such blocks (one set;
+      // the sort makes it one contiguous run per set) contributes exactly what ONE edge
+      // of that set with w' summed over the run does: the run is replaced by a
+      // representative edge in the bucket N + k below.  Uniform-weight buckets give it
+      // w' x (edges of the run); otherwise the run's weights move to the M = 0 weight
+      // column, which m0sum_kernel sums into the representative's weight every apply.
+      // The kept blocks are compacted in order and the bucket is re-padded to whole tiles.
       std::vector<uint8_t> nu;
       nu.reserve(tile_u[k].size());
       int64_t nkept = 0, kreal = 0;
@@ -651,6 +665,89 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<double>().swap(wrow);
   std::vector<int32_t>().swap(newid);
 
+  // ---- representatives of the M = 0 runs: bucket N + k holds one edge per size-k run
+  // (distinct sets, already in sorted order); weight slot wpos of each non-uniform one
+  // is written by m0sum_kernel every apply from its run's chunks of h_w0
+  std::vector<long long> h_m0job;    // m0sum_kernel jobs: (x, y) pairs (kernels.cu)
+  std::vector<long long> h_pentry;   // per short run of a pack: (wpos << 18) | (offset << 9) | length
+  std::vector<int64_t> h_rc0;        // per split run (several chunk jobs): its first and end job
+  std::vector<int64_t> h_wpos;       // per split run: its representative's weight slot
+  struct WRun { int64_t a, b, wpos; };
+  std::vector<WRun> wruns;
+  if (!m0runs.empty()) {
+    // m0sum_kernel jobs: a run of > kShort weights is cut into chunks of <= kChunk, one
+    // warp each; a shorter run is one thread's job
+    constexpr int64_t kChunk = 2048, kShort = 256;
+    const int epl = p->ent.epl, wblock = 32 * epl;
+    for (int k = 1; k <= N; ++k) {
+      const int bi = N + k;
+      int64_t nrep = 0;
+      for (const M0Run& r : m0runs) nrep += r.k == k;
+      if (nrep == 0) continue;
+      mk[bi] = nrep;
+      stride[bi] = (nrep + tile - 1) / tile * tile;
+      ids_off[bi] = ids_total;
+      w_off[bi] = w_total;
+      ids_total += (int64_t)k * stride[bi];
+      w_total += stride[bi];
+      h_ids.resize((size_t)ids_total, 0);
+      h_w.resize((size_t)w_total, 0.0);
+      int32_t* col = h_ids.data() + ids_off[bi];
+      const int64_t st = stride[bi];
+      int64_t j = 0;
+      for (const M0Run& r : m0runs) {
+        if (r.k != k) continue;
+        for (int q = 0; q < k; ++q) col[(int64_t)q * st + j] = m0ids[r.ids + q];
+        if (wuni[k]) {
+          h_w[w_off[bi] + j] = (double)((long double)wconst[k] * (long double)r.cnt);
+        } else {
+          // the lane-major layout (below) moves sorted position j of a warp block
+          const int64_t b0 = j / wblock * wblock, in = j % wblock;
+          wruns.push_back(WRun{r.w0, r.w1, w_off[bi] + b0 + (in % epl) * 32 + in / epl});
+        }
+        ++j;
+      }
+      for (; j < st; ++j) {  // padding: weight-0 copies of the last representative
+        for (int q = 0; q < k; ++q) col[(int64_t)q * st + j] = col[(int64_t)q * st + nrep - 1];
+        h_w[w_off[bi] + j] = 0.0;
+      }
+      stored[bi] = nrep;
+      wuni[bi] = 0;
+      tile_u[bi].assign(st / tile * nblk, 0);
+      block_u(k, col, st, tile_u[bi]);
+      p->m0_groups += nrep;
+    }
+    // one warp job each: a run of <= kChunk weights (y = its weight slot); a chunk of a
+    // longer run (y = -1 - run: partial sum + fold); a pack of neighbouring short runs
+    // (<= kShort weights each, adjacent in h_w0, <= kShort in all; y = (first entry << 9) | runs)
+    constexpr long long kPack = 1ll << 62;
+    auto job = [&](long long x, long long y) { h_m0job.push_back(x); h_m0job.push_back(y); };
+    for (size_t q = 0; q < wruns.size();) {
+      const WRun& wr = wruns[q];
+      const int64_t n = wr.b - wr.a;
+      if (n > kShort) {
+        if (n <= kChunk) {
+          job(((long long)wr.a << 24) | n, wr.wpos);
+        } else {
+          const long long run = (long long)h_wpos.size();
+          h_rc0.push_back((int64_t)(h_m0job.size() / 2));
+          for (int64_t a = wr.a; a < wr.b; a += kChunk) job(((long long)a << 24) | std::min<int64_t>(kChunk, wr.b - a), -1 - run);
+          h_rc0.push_back((int64_t)(h_m0job.size() / 2));
+          h_wpos.push_back(wr.wpos);
+        }
+        ++q;
+        continue;
+      }
+      size_t q1 = q + 1;
+      while (q1 < wruns.size() && wruns[q1].a == wruns[q1 - 1].b && wruns[q1].b - wr.a <= kShort) ++q1;
+      job(kPack | ((long long)wr.a << 24) | (wruns[q1 - 1].b - wr.a), ((long long)h_pentry.size() << 9) | (long long)(q1 - q));
+      for (size_t i = q; i < q1; ++i)
+        h_pentry.push_back(((long long)wruns[i].wpos << 18) | ((wruns[i].a - wr.a) << 9) | (wruns[i].b - wruns[i].a));
+      q = q1;
+    }
+    p->m0_chunks = (int64_t)(h_m0job.size() / 2);
+  }
+
   // ---- tile order: buckets most expensive first (the dynamic scheduler's tail is the cheapest work)
   int occ = 0;
   int hot = 256;  // ids below H accumulate in per-CTA L2 slices (STTSV_HOT overrides, for experiments;
@@ -667,17 +764,17 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
     if (e0 != cudaSuccess) { free_plan(p); return cuda_fail(e0, "edge kernel configuration"); }
     if (occ < 1) { free_plan(p); return fail(STTSV_ERR_CUDA, "edge kernel cannot be resident (smem %zu)", p->smem); }
   }
-  std::vector<int> order;
-  for (int k = 1; k <= N; ++k)
-    if (mk[k] > 0) order.push_back(k);
+  std::vector<int> order;  // bucket indices in kernel order
+  for (int bi = 1; bi <= NB; ++bi)
+    if (stored[bi] > 0) order.push_back(bi);
   // per-edge cost of a bucket as the kernel will execute it (the shared-prefix memo
   // makes most of a bucket cheap; its unshared blocks cost the full DP)
-  std::vector<double> ecost(N + 1, 0.0);
-  for (int k = 1; k <= N; ++k) {
-    if (mk[k] == 0) continue;
+  std::vector<double> ecost(NB + 1, 0.0);
+  for (int bi : order) {
+    const int k = ksz(bi);
     double c = 0;
-    for (size_t bl = 0; bl < tile_u[k].size(); ++bl) c += dp_fma_prefix(N, k, tile_u[k][bl]);
-    ecost[k] = tile_u[k].empty() ? dp_fma(N, k) : c / (double)tile_u[k].size();
+    for (size_t bl = 0; bl < tile_u[bi].size(); ++bl) c += dp_fma_prefix(N, k, tile_u[bi][bl]);
+    ecost[bi] = tile_u[bi].empty() ? dp_fma(N, k) : c / (double)tile_u[bi].size();
   }
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ecost[a] > ecost[b]; });
   EdgeKernelParams& kp = p->kp;
@@ -685,41 +782,43 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   kp.nb = (int)order.size();
   int64_t tiles = 0;
   double fma = 0;
-  for (int i = 0; i < kp.nb; ++i) {
-    const int k = order[i];
-    BucketDesc& b = kp.b[i];
-    b.k = k;
-    b.m = stored[k];
-    b.stride = stride[k];
-    b.tile_begin = tiles;
-    b.ids_off = ids_off[k];
-    b.w_off = w_off[k];
-    b.wuni = wuni[k];
-    b.wc = wconst[k];
-    tiles += (stored[k] + tile - 1) / tile;
+  for (int k = 1; k <= N; ++k) {  // input edges: in the stream or in an M = 0 run
     fma += dp_fma(N, k) * (double)(stored[k] + m0cnt[k]);
     p->stored_edges += stored[k] + m0cnt[k];
     p->stored_inc += (stored[k] + m0cnt[k]) * k;
     p->m0_edges += m0cnt[k];
-    p->prefix_inc += m0cnt[k] * k;
     if (!wuni[k]) p->stream_bytes += m0cnt[k] * 8;  // the M = 0 weights m0sum_kernel reads
-    const int64_t ntl = (stored[k] + tile - 1) / tile;
+  }
+  for (int i = 0; i < kp.nb; ++i) {
+    const int bi = order[i], k = ksz(bi);
+    BucketDesc& b = kp.b[i];
+    b.k = k;
+    b.m = stored[bi];
+    b.stride = stride[bi];
+    b.tile_begin = tiles;
+    b.ids_off = ids_off[bi];
+    b.w_off = w_off[bi];
+    b.wuni = wuni[bi];
+    b.wc = wconst[bi];
+    tiles += (stored[bi] + tile - 1) / tile;
+    const int64_t ntl = (stored[bi] + tile - 1) / tile;
     for (int64_t tl = 0; tl < ntl; ++tl) {
       int us = k;  // staged columns: from the smallest prefix of the tile's blocks
-      for (int w = 0; w < nblk; ++w) us = std::min<int>(us, tile_u[k][tl * nblk + w]);
-      p->stream_bytes += (int64_t)tile * (idb * (k - us) + (wuni[k] ? 0 : 8));
+      for (int w = 0; w < nblk; ++w) us = std::min<int>(us, tile_u[bi][tl * nblk + w]);
+      p->stream_bytes += (int64_t)tile * (idb * (k - us) + (wuni[bi] ? 0 : 8));
       for (int w = 0; w < nblk; ++w) {
-        const int u = tile_u[k][tl * nblk + w];
+        const int u = tile_u[bi][tl * nblk + w];
         const int64_t first = tl * tile + (int64_t)w * wblk;
-        const int64_t real = std::max<int64_t>(0, std::min<int64_t>(wblk, stored[k] - first));  // not padding
+        const int64_t real = std::max<int64_t>(0, std::min<int64_t>(wblk, stored[bi] - first));  // not padding
         p->fma_exec += dp_fma_prefix(N, k, u) * (double)real;
         if (u > 0) {
           p->prefix_tiles += 1;
-          p->prefix_inc += (int64_t)u * real;
+          if (bi <= N) p->prefix_inc += (int64_t)u * real;
         }
       }
     }
   }
+  for (int k = 1; k <= N; ++k) p->prefix_inc += m0cnt[k] * k;  // M = 0 runs: every member is shared
   kp.num_tiles = tiles;
   // shared-prefix groups: consecutive tiles (kernel order) with the same bucket, U and
   // prefix ids share a group id; U = 0 tiles have none (-1)
@@ -729,32 +828,29 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   std::vector<double> h_gtab;  // group records (prefix.cuh): [A: L][C: U x L][ids: U]; ids filled here
   std::vector<long long> h_items;  // group_kernel work items: (group << 8) | prefix member
   std::map<std::vector<int32_t>, int32_t> gmap;
-  std::vector<double> h_gm0w;          // per group: w' x edges of its uniform-weight M = 0 runs
-  std::vector<int64_t> h_gcoff;        // per group: first chunk (+ end sentinel)
-  std::vector<long long> h_m0chunk;    // per chunk: (first weight << 13) | length
-  if (memo && (p->prefix_tiles > 0 || !m0runs.empty())) {
+  if (memo && p->prefix_tiles > 0) {
     h_hdr.assign((size_t)tiles * (1 + nblk), 0);
     int32_t gid = -1;
     int pk = -1, pu = -1;
     std::vector<int32_t> pref, cur;
     for (int i = 0; i < kp.nb; ++i) {
-      const int k = kp.b[i].k;
-      const int32_t* col = h_ids.data() + ids_off[k];
-      const int64_t ntl = (stored[k] + tile - 1) / tile;
+      const int bi = order[i], k = kp.b[i].k;
+      const int32_t* col = h_ids.data() + ids_off[bi];
+      const int64_t ntl = (stored[bi] + tile - 1) / tile;
       for (int64_t tl = 0; tl < ntl; ++tl) {
         const int64_t t = kp.b[i].tile_begin + tl;
         int us = k;
-        for (int w = 0; w < nblk; ++w) us = std::min<int>(us, tile_u[k][tl * nblk + w]);
+        for (int w = 0; w < nblk; ++w) us = std::min<int>(us, tile_u[bi][tl * nblk + w]);
         h_hdr[(size_t)t * (1 + nblk)] = us;
         for (int w = 0; w < nblk; ++w) {
-          const int u = tile_u[k][tl * nblk + w];
+          const int u = tile_u[bi][tl * nblk + w];
           if (u == 0) {
             pk = -1;
             continue;
           }
           const int64_t j0 = tl * tile + (int64_t)w * wblk;
           cur.assign(u, 0);
-          for (int q = 0; q < u; ++q) cur[q] = col[(int64_t)q * stride[k] + j0];
+          for (int q = 0; q < u; ++q) cur[q] = col[(int64_t)q * stride[bi] + j0];
           if (!(k == pk && u == pu && cur == pref)) {
             pk = k;
             pu = u;
@@ -781,62 +877,6 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
           h_hdr[(size_t)t * (1 + nblk) + 1 + w] = ((long long)h_goff[gid] << 8) | u;
         }
       }
-    }
-    // M = 0 runs: a group per distinct vertex set (U = k: all members are prefix members)
-    std::vector<std::vector<std::pair<int64_t, int64_t>>> granges;  // per group: its M = 0 weight ranges
-    std::vector<long double> gm0(h_gku.size(), 0.0L);
-    granges.resize(h_gku.size());
-    for (const M0Run& r : m0runs) {
-      const int k = r.k;
-      std::vector<int32_t> key(m0ids.begin() + r.ids, m0ids.begin() + r.ids + k);
-      key.push_back(k);
-      key.push_back(k);
-      int32_t gid;
-      auto f = gmap.find(key);
-      if (f != gmap.end()) {
-        gid = f->second;
-      } else {
-        gid = (int32_t)h_gku.size();
-        gmap.emplace(key, gid);
-        const int L = N - k + 1;
-        h_gku.push_back(k | (k << 8));
-        h_goff.push_back((int64_t)h_gtab.size());
-        h_gtab.resize(h_gtab.size() + L + (size_t)k * L + k, 0.0);
-        long long* ids = reinterpret_cast<long long*>(h_gtab.data() + h_gtab.size() - k);
-        for (int q = 0; q < k; ++q) ids[q] = key[q];
-        for (int q = 0; q < k; ++q) h_items.push_back(((long long)gid << 8) | q);
-        gm0.push_back(0.0L);
-        granges.emplace_back();
-      }
-      if (wuni[k]) gm0[gid] += (long double)wconst[k] * (long double)r.cnt;
-      else if (r.w1 > r.w0) granges[gid].push_back({r.w0, r.w1});
-    }
-    h_gm0w.resize(h_gku.size());
-    h_gcoff.resize(h_gku.size() + 1);
-    constexpr int64_t kChunk = 4096;  // weights per m0sum_kernel chunk (a warp each)
-    for (size_t g = 0; g < h_gku.size(); ++g) {
-      h_gm0w[g] = (double)gm0[g];
-      h_gcoff[g] = (int64_t)h_m0chunk.size();
-      for (const auto& rg : granges[g])
-        for (int64_t a = rg.first; a < rg.second; a += kChunk)
-          h_m0chunk.push_back(((long long)a << 13) | (long long)std::min<int64_t>(kChunk, rg.second - a));
-      if (h_gm0w[g] != 0.0 || h_gcoff[g] < (int64_t)h_m0chunk.size()) ++p->m0_groups;
-    }
-    h_gcoff[h_gku.size()] = (int64_t)h_m0chunk.size();
-    p->m0_chunks = (int64_t)h_m0chunk.size();
-    // group_kernel items ordered by the prefix member's vertex, so a warp's M = 0
-    // deposits to one vertex (the hottest are in most groups) aggregate into one red
-    {
-      std::vector<std::pair<long long, long long>> keyed(h_items.size());
-      for (size_t t = 0; t < h_items.size(); ++t) {
-        const int64_t g = h_items[t] >> 8;
-        const int i = (int)(h_items[t] & 255);
-        const int k = h_gku[g] & 255, u = h_gku[g] >> 8, L = N - k + 1;
-        const long long v = reinterpret_cast<const long long*>(h_gtab.data() + h_goff[g] + L + (size_t)u * L)[i];
-        keyed[t] = {v, h_items[t]};
-      }
-      std::stable_sort(keyed.begin(), keyed.end());
-      for (size_t t = 0; t < h_items.size(); ++t) h_items[t] = keyed[t].second;
     }
     p->prefix_groups = (int64_t)h_gku.size();
     // the group kernel is instantiated up to the largest L of the plan's groups (kernels.cu)
@@ -953,11 +993,13 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   const size_t b_tu = align(h_hdr.size() * 8 + 8), b_tg = 0;
   const size_t b_gku = align(h_gku.size() * 4 + 4), b_goff = align(h_goff.size() * 8 + 8),
                b_gtab = align(h_gtab.size() * 8 + 8), b_items = align(h_items.size() * 8 + 8);
-  const size_t b_gm0w = align(h_gm0w.size() * 8 + 8), b_gcoff = align(h_gcoff.size() * 8 + 8),
-               b_m0chunk = align(h_m0chunk.size() * 8 + 8), b_w0 = align(h_w0.size() * 8 + 8),
-               b_m0sum = align(h_m0chunk.size() * 8 + 8);
+  const size_t b_m0chunk = align(h_m0job.size() * 8 + 16), b_crun = align(h_pentry.size() * 8 + 8),
+               b_rc0 = align(h_rc0.size() * 8 + 8), b_wpos = align(h_wpos.size() * 8 + 8),
+               b_w0 = align(h_w0.size() * 8 + 8), b_part = align(h_m0job.size() / 2 * 8 + 8),
+               b_rcnt = align(h_wpos.size() * 4 + 4);
+  const size_t b_m0 = b_m0chunk + b_crun + b_rc0 + b_wpos + b_w0 + b_part + b_rcnt;
   p->dbytes = b_ids + b_w + b_act + b_xa + b_ya + b_scr + b_xg + b_cta + b_priv + b_tu + b_tg + b_gku + b_goff + b_gtab +
-              b_items + b_gm0w + b_gcoff + b_m0chunk + b_w0 + b_m0sum;
+              b_items + b_m0;
   cudaError_t ce = cudaMalloc(&p->dmem, p->dbytes);
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "cudaMalloc plan"); }
   char* base = (char*)p->dmem;
@@ -977,11 +1019,13 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   double* d_gtab = (double*)(gbase + b_gku + b_goff);
   long long* d_items = (long long*)(gbase + b_gku + b_goff + b_gtab);
   char* mbase = gbase + b_gku + b_goff + b_gtab + b_items;
-  double* d_gm0w = (double*)mbase;
-  int64_t* d_gcoff = (int64_t*)(mbase + b_gm0w);
-  long long* d_m0chunk = (long long*)(mbase + b_gm0w + b_gcoff);
-  double* d_w0 = (double*)(mbase + b_gm0w + b_gcoff + b_m0chunk);
-  p->d_m0sum = (double*)(mbase + b_gm0w + b_gcoff + b_m0chunk + b_w0);
+  long long* d_m0job = (long long*)mbase;
+  long long* d_pentry = (long long*)(mbase + b_m0chunk);
+  int64_t* d_rc0 = (int64_t*)(mbase + b_m0chunk + b_crun);
+  int64_t* d_wpos = (int64_t*)(mbase + b_m0chunk + b_crun + b_rc0);
+  double* d_w0 = (double*)(mbase + b_m0chunk + b_crun + b_rc0 + b_wpos);
+  p->d_m0part = (double*)(mbase + b_m0chunk + b_crun + b_rc0 + b_wpos + b_w0);
+  p->d_m0cnt = (unsigned int*)(mbase + b_m0chunk + b_crun + b_rc0 + b_wpos + b_w0 + b_part);
   p->gs = gs;
   if (ids_total && idb == 4) ce = cudaMemcpy(d_ids, h_ids.data(), ids_total * 4, cudaMemcpyHostToDevice);
   if (ids_total && idb == 2) {
@@ -997,14 +1041,20 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (ce == cudaSuccess && !h_gtab.empty()) ce = cudaMemcpy(d_gtab, h_gtab.data(), h_gtab.size() * 8, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && !h_items.empty())
     ce = cudaMemcpy(d_items, h_items.data(), h_items.size() * 8, cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess && !h_gm0w.empty()) ce = cudaMemcpy(d_gm0w, h_gm0w.data(), h_gm0w.size() * 8, cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess && !h_gcoff.empty()) ce = cudaMemcpy(d_gcoff, h_gcoff.data(), h_gcoff.size() * 8, cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess && !h_m0chunk.empty())
-    ce = cudaMemcpy(d_m0chunk, h_m0chunk.data(), h_m0chunk.size() * 8, cudaMemcpyHostToDevice);
-  if (ce == cudaSuccess && !h_w0.empty()) ce = cudaMemcpy(d_w0, h_w0.data(), h_w0.size() * 8, cudaMemcpyHostToDevice);
-  p->d_gm0w = h_gm0w.empty() ? nullptr : d_gm0w;
-  p->d_gcoff = h_gcoff.empty() ? nullptr : d_gcoff;
-  p->d_m0chunk = d_m0chunk;
+  if (ce == cudaSuccess && !h_m0job.empty()) {
+    ce = cudaMemcpy(d_m0job, h_m0job.data(), h_m0job.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess && !h_pentry.empty())
+      ce = cudaMemcpy(d_pentry, h_pentry.data(), h_pentry.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(d_rc0, h_rc0.data(), h_rc0.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess && !h_wpos.empty())
+      ce = cudaMemcpy(d_wpos, h_wpos.data(), h_wpos.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(d_w0, h_w0.data(), h_w0.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess && !h_wpos.empty()) ce = cudaMemset(p->d_m0cnt, 0, h_wpos.size() * 4);
+  }
+  p->d_m0job = d_m0job;
+  p->d_pentry = d_pentry;
+  p->d_rc0 = d_rc0;
+  p->d_wpos = d_wpos;
   p->d_w0 = d_w0;
   p->d_items = d_items;
   p->nitems = (int64_t)h_items.size();
@@ -1019,6 +1069,7 @@ extern "C" sttsv_status_t sttsv_plan_create(sttsv_plan_t* out, int64_t n, int32_
   if (ce != cudaSuccess) { free_plan(p); return cuda_fail(ce, "plan upload"); }
   kp.ids = d_ids;
   kp.w = d_w;
+  p->d_wpool = d_w;
   kp.xa = p->d_xa;
   kp.xg = p->d_xg;
   kp.gs = gs;
@@ -1136,6 +1187,13 @@ static sttsv_status_t check_async(sttsv_plan_s* p) {
   return STTSV_OK;
 }
 
+// the M = 0 runs' representative weights (x-independent; a no-op for plans without runs
+// of non-uniform weights)
+static cudaError_t launch_m0(sttsv_plan_s* p, cudaStream_t s) {
+  return launch_m0sum(p->d_w0, p->d_m0job, p->m0_chunks, p->d_pentry, p->d_rc0, p->d_wpos, p->d_m0part, p->d_m0cnt,
+                      p->d_wpool, s);
+}
+
 // y_a = (B x_a^{N-1}) on the active vertices (x_a already gathered)
 // zeroed: the prologue kernel, launched just before on `s`, cleared y_a; the
 // edge kernel is then a programmatic dependent launch (kernels.cu)
@@ -1143,7 +1201,7 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
   if (p->n_active == 0) return STTSV_OK;
   if (!p->det && !zeroed) CUDA_TRY(cudaMemsetAsync(p->d_ya, 0, p->n_active * sizeof(double), s), "memset y_a");
   const bool groups = p->kp.gtab != nullptr;
-  if (p->kp.num_tiles > 0 || groups) {
+  if (p->kp.num_tiles > 0) {
     std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
     if (p->profiling) {
       if (p->events_used == p->events.size()) {
@@ -1157,15 +1215,12 @@ static sttsv_status_t apply_active(sttsv_plan_s* p, cudaStream_t s, bool zeroed 
     }
     // the M = 0 runs' weight sums (x-independent; prefix.cuh), then the per-apply
     // shared-prefix group table with the M = 0 deposits (prefix.cuh)
-    if (p->m0_chunks > 0)
-      CUDA_TRY(launch_m0sum(p->d_w0, p->d_m0chunk, p->m0_chunks, p->d_m0sum, s), "m0sum launch");
+    if (p->m0_chunks > 0) CUDA_TRY(launch_m0(p, s), "m0sum launch");
     if (groups)
       CUDA_TRY(launch_groups(p->d_xg, p->gs, p->N, p->d_gku, p->d_goff, p->d_items, p->nitems, p->group_lmax,
-                             p->kp.gtab, const_cast<double*>(p->kp.gtab), p->d_gm0w, p->d_gcoff, p->d_m0sum,
-                             p->d_ya, s), "group kernel launch");
-    if (p->kp.num_tiles > 0)
-      CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0,
-                                  groups || (zeroed && p->m0_chunks == 0)), "edge kernel launch");
+                             p->kp.gtab, const_cast<double*>(p->kp.gtab), s), "group kernel launch");
+    CUDA_TRY(launch_edge_kernel(p->ent, p->kp, p->grid, p->smem, s, p->det ? 2 : 0,
+                                groups || (zeroed && p->m0_chunks == 0)), "edge kernel launch");
     if (ev) CUDA_TRY(cudaEventRecord(ev->second, s), "cudaEventRecord");
   }
   if (p->det)  // fixed-order sums of the vertex-major buffer (every active vertex written)
@@ -1399,7 +1454,8 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
                            p->gs, p->ent.table_norm, na, s), "gather launch");
   if (na > 0) {
     CUDA_TRY(cudaMemsetAsync(p->b_ya, 0, (size_t)nvec * na * sizeof(double), s), "memset y_a");
-    if (p->kp.num_tiles > 0 || p->kp.gtab) {
+    if (p->m0_chunks > 0) CUDA_TRY(launch_m0(p, s), "m0sum launch");
+    if (p->kp.num_tiles > 0) {
       EdgeKernelParams kp = p->kp;
       kp.nvec = nvec;
       kp.xa = p->b_xa;
@@ -1411,20 +1467,16 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       // shared-prefix memo: one group table per vector (prefix.cuh)
       const bool groups = p->kp.gtab != nullptr;
       if (groups) {
-        if (p->m0_chunks > 0)
-          CUDA_TRY(launch_m0sum(p->d_w0, p->d_m0chunk, p->m0_chunks, p->d_m0sum, s), "m0sum launch");
         for (int v = 0; v < nvec; ++v)
           CUDA_TRY(launch_groups(p->b_xg + (size_t)v * na * p->gs, p->gs, p->N, p->d_gku, p->d_goff, p->d_items,
-                                 p->nitems, p->group_lmax, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles,
-                                 p->d_gm0w, p->d_gcoff, p->d_m0sum, p->b_ya + (size_t)v * na, s),
+                                 p->nitems, p->group_lmax, p->kp.gtab, p->b_gtab + (size_t)v * p->gtab_doubles, s),
                    "group kernel launch");
         kp.gtab = p->b_gtab;
         kp.gtab_vstride = p->gtab_doubles;
       }
       kp.group_wait = groups;
-      if (p->kp.num_tiles > 0)
-        CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0), groups),
-                 "edge kernel launch");
+      CUDA_TRY(launch_edge_kernel(p->ent, kp, p->grid, p->smem, s, nvec > 1 ? 1 : (p->det ? 2 : 0), groups),
+               "edge kernel launch");
       if (p->det) CUDA_TRY(launch_det_reduce(p->d_contrib, p->d_cstart, p->det_chunks, p->d_csum, p->d_vchunk,
                                              p->b_ya, na, s), "deterministic reduce launch");
     }

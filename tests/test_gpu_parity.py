@@ -581,9 +581,9 @@ def test_prefix_memo(S, torch_cuda, N, kmax):
 # ------------------------------------------ M = 0 runs (prefix.cuh: one repeated vertex set)
 @pytest.mark.parametrize("N,uniform", [(5, True), (5, False), (8, True), (12, False), (25, True), (25, False)])
 def test_m0_runs(S, torch_cuda, N, uniform):
-    """Long runs of one repeated vertex set leave the tile stream (plan info m0_edges); the
-    group kernel deposits C_i[0] times the run's summed w' (a plan-time count for uniform
-    weights, per-apply chunk sums of the stored weights otherwise).  Against the oracle on
+    """Long runs of one repeated vertex set leave the tile stream (plan info m0_edges); each
+    run becomes one representative edge with the run's summed w' (a plan-time count for
+    uniform weights, per-apply chunk sums of the stored weights otherwise).  Against the oracle on
     the same hypergraph, through apply, the batched apply (both strategies) and 3 power steps."""
     torch = torch_cuda
     rng = np.random.default_rng(700 + N + 1000 * uniform)
@@ -626,7 +626,8 @@ def test_m0_runs(S, torch_cuda, N, uniform):
 
 
 def test_m0_only_plan(S, torch_cuda):
-    """Every edge the same vertex set: no tile stream at all (num_tiles 0), only the group kernel."""
+    """Every edge one of two vertex sets: the stream holds only the two runs' representatives
+    (one tile per size)."""
     torch = torch_cuda
     edges = [[3, 7, 11]] * 5000 + [[2]] * 3000
     rng = np.random.default_rng(5)
@@ -635,7 +636,7 @@ def test_m0_only_plan(S, torch_cuda):
         hg = to_hg(20, 6, edges, w, rng.uniform(0.05, 1.0, 20))
         plan = S.Plan.from_hypergraph(hg)
         info = plan.info()
-        assert info["num_tiles"] == 0 and info["m0_edges"] == len(edges), info
+        assert info["num_tiles"] == 2 and info["m0_edges"] == len(edges) and info["m0_groups"] == 2, info
         y = plan.apply(torch.from_numpy(hg.x).cuda()).cpu().numpy()
         assert rel(y, oracle.sttsv(hg)) < TOL
         plan.close()
