@@ -112,6 +112,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef STTSV_PIPE_ML
 #define STTSV_PIPE_ML 8
 #endif
+// prefix blocks: the flush's C rows are loaded into registers at the start of the
+// block for L <= FLUSHPRE_L8 (N <= 8) / FLUSHPRE_L (larger N, where registers are short)
+#ifndef STTSV_FLUSHPRE_L8
+#define STTSV_FLUSHPRE_L8 32
+#endif
+#ifndef STTSV_FLUSHPRE_L
+#define STTSV_FLUSHPRE_L 3
+#endif
 #ifndef STTSV_SLOTS
 #define STTSV_SLOTS 16
 #endif
@@ -600,16 +608,20 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
     double a[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) a[j] = __ldg(G + j);  // front A (row format), the same on every lane
-    // the flush's rows: lane i < U takes prefix member i's C_i and id now (U <= 31)
-    double cpre[L];
+    // the flush's rows: lane i < U takes prefix member i's C_i and id now (U <= 31),
+    // where the registers allow it (FLUSHPRE)
+    constexpr bool FLUSHPRE = L <= (N <= 8 ? STTSV_FLUSHPRE_L8 : STTSV_FLUSHPRE_L);
+    double cpre[FLUSHPRE ? L : 1];
     int vpre = -1;
-    if (lane < U) {
+    if constexpr (FLUSHPRE) {
+      if (lane < U) {
 #pragma unroll
-      for (int j = 0; j < L; ++j) cpre[j] = __ldg(G + L + lane * L + j);
-      vpre = (int)__ldg(reinterpret_cast<const long long*>(G + L + U * L) + lane);
-    } else {
+        for (int j = 0; j < L; ++j) cpre[j] = __ldg(G + L + lane * L + j);
+        vpre = (int)__ldg(reinterpret_cast<const long long*>(G + L + U * L) + lane);
+      } else {
 #pragma unroll
-      for (int j = 0; j < L; ++j) cpre[j] = 0.0;
+        for (int j = 0; j < L; ++j) cpre[j] = 0.0;
+      }
     }
     // Runs of identical consecutive edges among the lane's EPL edges (sorted
     // buckets keep duplicates adjacent) need one DP each, on the run's summed
@@ -731,7 +743,8 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
       }
     }
     __syncwarp();  // the queue is read before the reduction reuses the scratch
-    prefix_tile_flush_pre<L>(sb, sred, cpre, vpre, sk, lane);
+    if constexpr (FLUSHPRE) prefix_tile_flush_pre<L>(sb, sred, cpre, vpre, sk, lane);
+    else prefix_tile_flush<L>(sb, sred, G, U, sk, lane);
   }
 }
 
