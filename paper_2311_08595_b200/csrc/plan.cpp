@@ -1449,6 +1449,21 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
     p->b_gtab = (double*)(b + 2 * a + gbytes + pr);
     p->batch_cap = nvec;
   }
+  // the zero-fill of the dense outputs (8n bytes per vector) on the side stream,
+  // overlapping the edge kernel (as apply_dense)
+  const bool fork = p->kp.num_tiles > 0;
+  if (fork) {
+    if (!p->side) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking), "side stream");
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "event");
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "event");
+    }
+    CUDA_TRY(cudaEventRecord(p->ev_fork, s), "fork record");
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0), "fork wait");
+  }
+  CUDA_TRY(cudaMemset2DAsync(Y, (size_t)ld * sizeof(double), 0, (size_t)p->n * sizeof(double), (size_t)nvec,
+                             fork ? p->side : s), "memset Y");
+  if (fork) CUDA_TRY(cudaEventRecord(p->ev_join, p->side), "join record");
   for (int v = 0; v < nvec; ++v)
     CUDA_TRY(launch_gather(X + (size_t)v * ld, p->d_act, p->b_xa + (size_t)v * na, p->b_xg + (size_t)v * na * p->gs,
                            p->gs, p->ent.table_norm, na, s), "gather launch");
@@ -1487,8 +1502,8 @@ extern "C" sttsv_status_t sttsv_apply_batch(sttsv_plan_t p, const double* X, dou
       ++p->allreduces;
     }
   }
+  if (fork) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0), "join wait");
   for (int v = 0; v < nvec; ++v) {
-    CUDA_TRY(cudaMemsetAsync(Y + (size_t)v * ld, 0, (size_t)p->n * sizeof(double), s), "memset Y");
     CUDA_TRY(launch_expand(p->b_ya + (size_t)v * na, p->d_act, Y + (size_t)v * ld, na, s), "expand launch");
   }
   return STTSV_OK;
