@@ -476,12 +476,12 @@ __device__ __forceinline__ void slots_deposit_off(const int (&id)[M], const doub
 // sum_j C_i[j] T[j] (lane i < U).  L <= 2: shuffle butterfly; else a transpose
 // through this warp's shared-memory rows sred (row j = term j of the 32 lanes,
 // kRedStride apart: conflict-free 16-byte reads).
-template <int L>
+template <int L, bool SHFL = false>
 __device__ __forceinline__ void prefix_tile_flush(double (&sb)[L], double* sred, const double* __restrict__ G, int U,
                                                   const Sink& sk, int lane) {
   const double* C = G + L;
   const long long* pid = reinterpret_cast<const long long*>(G + L + U * L);
-  if constexpr (L <= 2) {
+  if constexpr (L <= 2 || SHFL) {
 #pragma unroll
     for (int j = 0; j < L; ++j)
 #pragma unroll
@@ -522,10 +522,10 @@ __device__ __forceinline__ void prefix_tile_flush(double (&sb)[L], double* sred,
 // prefix_tile_flush with the prefix members' rows prefetched at the start of the
 // block (lane i < U holds C_i in c[] and the member's id in v; U <= 31 here): the
 // flush does not wait on the group table
-template <int L>
+template <int L, bool SHFL = false>
 __device__ __forceinline__ void prefix_tile_flush_pre(double (&sb)[L], double* sred, const double (&c)[L], int v,
                                                       const Sink& sk, int lane) {
-  if constexpr (L <= 2) {
+  if constexpr (L <= 2 || SHFL) {
 #pragma unroll
     for (int j = 0; j < L; ++j)
 #pragma unroll
@@ -578,11 +578,15 @@ __device__ __forceinline__ void prefix_tile_flush0(double t0, const double* __re
 // rows C_i and the prefix ids).  Each lane accumulates SB = sum_e w'_e B_e over
 // its edges; at the end of the block the warp sums SB and lane i < U deposits
 // member i's total  sum_j C_i[j] SB[j].
-template <int N, int K, int M, int TILE, int EPL, int RMAX, typename IdT>
+// BATCH (f4, sttsv_apply_batch): called once per vector (vpass = 0, 1, ...) on
+// the same staged block; the run queue is built by pass 0 only (its length is
+// kept in qn) and read again by the later passes, so the block flush keeps its
+// reduction in registers instead of the queue's shared scratch.
+template <int N, int K, int M, int TILE, int EPL, int RMAX, typename IdT, bool BATCH = false>
 __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, const WSrc& sw,
                                                   int base, const double* __restrict__ xg,
                                                   const double* __restrict__ G, RunAcc<RMAX>& ra, const Sink& sk,
-                                                  double* sred, int lane) {
+                                                  double* sred, int lane, int vpass, int& qn) {
   constexpr int L = N - K + 1;
   constexpr int GS = series_stride(N);
   constexpr int U = K - M;
@@ -631,6 +635,8 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
     // (consecutive distinct edges: the deposit runs carry over).
     double* qw = sred;
     int* qc = reinterpret_cast<int*>(sred + 32 * EPL);
+    int Q;
+    if (!BATCH || vpass == 0) {
     int prev[M];
     int nrun = 0;
 #pragma unroll
@@ -651,7 +657,7 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
       const int t = __shfl_up_sync(kFull, incl, o);
       if (lane >= o) incl += t;
     }
-    const int Q = __shfl_sync(kFull, incl, 31);
+    Q = __shfl_sync(kFull, incl, 31);
     {
       int pos = incl - nrun, rc = -1;
       double acc = 0.0;
@@ -682,6 +688,10 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
       qc[pos] = rc;
     }
     __syncwarp();
+    qn = Q;
+    } else {
+      Q = qn;
+    }
     const int c = (Q + 31) >> 5;
     // one queue entry: the DP over the own members with the front A, the
     // deposits of the own members and the entry's SB term
@@ -743,35 +753,38 @@ __device__ __forceinline__ void warp_block_prefix(const IdT* __restrict__ sids, 
       }
     }
     __syncwarp();  // the queue is read before the reduction reuses the scratch
-    if constexpr (FLUSHPRE) prefix_tile_flush_pre<L>(sb, sred, cpre, vpre, sk, lane);
-    else prefix_tile_flush<L>(sb, sred, G, U, sk, lane);
+    if constexpr (FLUSHPRE) prefix_tile_flush_pre<L, BATCH>(sb, sred, cpre, vpre, sk, lane);
+    else prefix_tile_flush<L, BATCH>(sb, sred, G, U, sk, lane);
   }
 }
 
 // prefix tiles of bucket K: dispatch on the number of own members M = K - U
-template <int N, int K, int M, int MMAX, int TILE, int EPL, int RMAX, typename IdT>
+template <int N, int K, int M, int MMAX, int TILE, int EPL, int RMAX, typename IdT, bool BATCH>
 __device__ __forceinline__ void dispatch_m(int m, const IdT* sids, const WSrc& sw, int base, const double* xg,
                                            const double* G, RunAcc<RMAX>& ra, const Sink& sk, double* sred,
-                                           int lane) {
+                                           int lane, int vpass, int& qn) {
   if constexpr (M < K && M <= MMAX) {
     if (m == M) {
-      warp_block_prefix<N, K, M, TILE, EPL, RMAX, IdT>(sids, sw, base, xg, G, ra, sk, sred, lane);
+      warp_block_prefix<N, K, M, TILE, EPL, RMAX, IdT, BATCH>(sids, sw, base, xg, G, ra, sk, sred, lane, vpass, qn);
       return;
     }
-    dispatch_m<N, K, M + 1, MMAX, TILE, EPL, RMAX, IdT>(m, sids, sw, base, xg, G, ra, sk, sred, lane);
+    dispatch_m<N, K, M + 1, MMAX, TILE, EPL, RMAX, IdT, BATCH>(m, sids, sw, base, xg, G, ra, sk, sred, lane, vpass,
+                                                               qn);
   }
 }
 
-template <int N, int K, int MMAX, int TILE, int EPL, int RMAX, typename IdT>
+template <int N, int K, int MMAX, int TILE, int EPL, int RMAX, typename IdT, bool BATCH>
 __device__ __forceinline__ void dispatch_kp(int k, int U, const IdT* sids, const WSrc& sw, int base,
                                             const double* xg, const double* G, RunAcc<RMAX>& ra, const Sink& sk,
-                                            double* sred, int lane) {
+                                            double* sred, int lane, int vpass, int& qn) {
   if constexpr (K <= N) {
     if (k == K) {
-      dispatch_m<N, K, 0, MMAX, TILE, EPL, RMAX, IdT>(K - U, sids, sw, base, xg, G, ra, sk, sred, lane);
+      dispatch_m<N, K, 0, MMAX, TILE, EPL, RMAX, IdT, BATCH>(K - U, sids, sw, base, xg, G, ra, sk, sred, lane, vpass,
+                                                             qn);
       return;
     }
-    dispatch_kp<N, K + 1, MMAX, TILE, EPL, RMAX, IdT>(k, U, sids, sw, base, xg, G, ra, sk, sred, lane);
+    dispatch_kp<N, K + 1, MMAX, TILE, EPL, RMAX, IdT, BATCH>(k, U, sids, sw, base, xg, G, ra, sk, sred, lane, vpass,
+                                                             qn);
   }
 }
 
@@ -1414,6 +1427,7 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
         }
         // one pass per vector; with several vectors the runs of a pass are flushed
         // (warp-aggregated) at its end, with one they continue across tiles
+        int qn = 0;  // batch: the block's run-queue length (built by the first vector's pass)
         for (int v = 0; v < nvec; ++v) {
           const Sink skv{priv_cta + (size_t)v * p.H, p.ya + (size_t)v * p.ya_vstride, p.H};
           const double* xgv = p.xg + (size_t)v * p.xg_vstride;
@@ -1425,8 +1439,8 @@ __global__ void __launch_bounds__(EdgeCfg<N, IDB>::THREADS, EdgeCfg<N, IDB>::MIN
             if constexpr (PREFIX) {
               if (tu > 0) {
                 need_groups();
-                dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT>(k, tu, sids, sw, base, xgv, Gv, ra, skv, sred,
-                                                                   lane);
+                dispatch_kp<N, 1, Cfg::PMAX, TILE, EPL, RMAX, IdT, BATCH>(k, tu, sids, sw, base, xgv, Gv, ra, skv,
+                                                                          sred, lane, v, qn);
                 done = true;
               }
             }
