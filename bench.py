@@ -375,6 +375,38 @@ def run_ours(args):
                      if sparse_x else
                      "host perf_counter around synchronous sttsv_apply_host (pinned buffers)"}
 
+    # ---------------- the same call on a dense-active input (every vertex active: the whole x
+    # and y cross PCIe, 8n bytes each way); world = 1 only, not the headline
+    e2e_dense = None
+    if world == 1 and not args.no_dense_e2e:
+        dhg = W.generate("dense-active")
+        dplan = S.Plan.from_hypergraph(dhg, device=dev_index)
+        dinfo = dplan.info()
+        dxh = torch.from_numpy(dhg.x.copy()).pin_memory()
+        dyh = torch.empty(dhg.n, dtype=torch.float64).pin_memory()
+        dx_np, dy_np = dxh.numpy(), dyh.numpy()
+        for _ in range(3):
+            dplan.apply_host(dx_np, dy_np)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            dplan.apply_host(dx_np, dy_np)
+        d_s = (time.perf_counter() - t0) / e2e_steps
+        dx = torch.from_numpy(dhg.x).to(dev)
+        dy = torch.empty_like(dx)
+        d_dev_ms = time_loop(lambda: dplan.apply(dx, dy, stream))
+        dense_x = dinfo["n_active"] * 8 > dhg.n
+        e2e_dense = {"workload": "dense-active", "n": dhg.n, "m": dhg.m, "rank_Nk": dhg.rank,
+                     "incidences": dhg.incidences, "n_active": dinfo["n_active"],
+                     "value": dhg.incidences / d_s, "unit": UNIT, "ms_per_step": d_s * 1e3,
+                     "device_ms_per_step": d_dev_ms,
+                     "h2d_bytes_per_step": int(dhg.n * 8 if dense_x else dinfo["n_active"] * 8),
+                     "d2h_bytes_per_step": int(dhg.n * 8 if dense_x else dinfo["n_active"] * 8),
+                     "note": "sttsv_apply_host on tiny's recipe scaled up (uniform members: every vertex "
+                             "active), so x and y cross PCIe whole; device_ms_per_step = sttsv_apply on "
+                             "resident buffers"}
+        dplan.close()
+        del dplan, dx, dy, dxh, dyh, dhg
+
     # ---------------- roofline of the dominant kernel (edge kernel)
     # binding roof = the larger of (bytes the kernel actually streams / HBM peak) and
     # (FP64 flops / FP64 peak); the SURVEY.md 8(d) int32-id byte count is secondary
@@ -489,6 +521,7 @@ def run_ours(args):
                "hbm_gbs_step": (4 * hg.incidences + 8 * hg.m + 16 * info["n_active"] + 8 * hg.n)
                / (ms_step * 1e-3) / 1e9,
                "roofline": roofline, "memo": memo, "no_memo": nomemo, "cpu_baseline": cpu, "e2e": e2e,
+               "e2e_dense": e2e_dense,
                "merge_duplicates": merged, "batch": batch,
                "gpu_launches": plan.launches() * args.steps, "clocks": sampler.summary()}
         if shard_check is not None:
@@ -514,6 +547,7 @@ def main():
     ap.add_argument("--no-merge-report", action="store_true")
     ap.add_argument("--no-batch-report", action="store_true")
     ap.add_argument("--no-memo-report", action="store_true")
+    ap.add_argument("--no-dense-e2e", action="store_true")
     ap.add_argument("--no-comm", action="store_true",
                     help="N>1 harness without the NCCL data plane (ranks may share a GPU; host-side shard sum)")
     args = ap.parse_args()

@@ -135,3 +135,21 @@ def test_high_rank_small_x(S, torch_cuda):
     assert np.max(np.abs(ref)) > 0
     check_vector(y, ref, deg, "high-rank x*1e-7")
     plan.close()
+
+
+def test_dense_active_full(S, torch_cuda):
+    """Every vertex active (tiny's recipe scaled to n = 2e6, m = 8e6: uniform members, int32 ids,
+    no hot skew, so the scatter is almost all direct reds into y_a) — the workload of bench.py's
+    e2e_dense figure.  sttsv_apply on device buffers and sttsv_apply_host on host buffers (x and y
+    cross PCIe whole) both against the oracle, every vertex."""
+    torch = torch_cuda
+    hg = W.generate("dense-active")
+    deg = np.bincount(hg.indices, minlength=hg.n)
+    assert np.count_nonzero(deg) > 0.99 * hg.n
+    ref = oracle.sttsv(hg)
+    y, plan = gpu_apply(S, torch, hg)
+    check_vector(y, ref, deg, "dense-active apply")
+    yh = np.full(hg.n, np.nan)
+    plan.apply_host(hg.x, yh)
+    check_vector(yh, ref, deg, "dense-active apply_host")
+    plan.close()

@@ -104,6 +104,10 @@ CONFIGS = {
                     "const", (1.0, 0.0)),
     "centrality": Config("centrality", 5_000_000, 50_000_000, 12, "geometric", 0.3, 2, 12, "zipf", 2.0,
                          "uniform", power_iters=50),
+    # not a BASELINE config: tiny's recipe (uniform members) scaled up so that every vertex is
+    # active; bench.py's e2e_dense figure moves the whole x and y across PCIe on it
+    "dense-active": Config("dense-active", 2_000_000, 8_000_000, 5, "uniform", 0.0, 2, 5, "uniform", 0.0,
+                           "uniform", note="e2e with 8n bytes each way (not a BASELINE config)"),
 }
 
 
