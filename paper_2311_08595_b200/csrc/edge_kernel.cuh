@@ -107,6 +107,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef STTSV_DYN_BLOCKS
 #define STTSV_DYN_BLOCKS 1
 #endif
+// unroll factor of the per-lane edge loop of a full-DP warp block (2 lets the compiler overlap
+// one edge's row gathers with the previous edge's DP; costs registers)
+#ifndef STTSV_WB_UNROLL
+#define STTSV_WB_UNROLL 1
+#endif
 // software-pipelined queue loop of the shared-prefix blocks for M*L <= PIPE_ML
 // (the next entry's rows in flight during the current DP; more costs registers)
 #ifndef STTSV_PIPE_ML
@@ -409,7 +414,8 @@ __device__ __forceinline__ void warp_block(const IdT* __restrict__ sids, const W
                                            const DetSink& ds, int lane) {
   constexpr int L = N - K + 1;
   constexpr int GS = series_stride(N);
-#pragma unroll 1
+  constexpr int WBU = STTSV_WB_UNROLL;
+#pragma unroll WBU
   for (int r = 0; r < EPL; ++r) {
     const int col = base + r * 32 + lane;  // lane-major tile layout (plan.cpp): sorted edge base + lane*EPL + r
     int id[K];
