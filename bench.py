@@ -358,18 +358,28 @@ def run_ours(args):
     xh = torch.from_numpy(hg.x.copy()).pin_memory()
     yh = torch.empty(hg.n, dtype=torch.float64).pin_memory()
     xh_np, yh_np = xh.numpy(), yh.numpy()
-    plan.apply_host(xh_np, yh_np)
-    e2e_steps = max(1, min(args.steps, 10))
+    # warm-up: the host cores idle during the device-only phases above, and the first ~10 calls
+    # after an idle stretch run 3x slower while the OpenMP team and the core clocks come back
+    # (tools/e2e_diag.py: 0.99, 0.94, 0.83 ... 0.32 ms), so the e2e loop gets its own warm-up
+    e2e_warmup = max(args.warmup, 15)
+    for _ in range(e2e_warmup):
+        plan.apply_host(xh_np, yh_np)
+    e2e_steps = max(1, min(args.steps, 20))
     barrier()
+    e2e_each = []
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
+        t1 = time.perf_counter()
         plan.apply_host(xh_np, yh_np)
+        e2e_each.append(time.perf_counter() - t1)
     barrier()
     e2e_s = max_over_ranks([(time.perf_counter() - t0) / e2e_steps])[0]
     sparse_x = info["n_active"] * 8 <= hg.n   # sttsv_apply_host copies only x on the active vertices
     e2e = {"value": hg.incidences / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(info["n_active"] * 8 if sparse_x else xh.numel() * 8),
            "d2h_bytes_per_step": int(info["n_active"] * 8 if sparse_x else yh.numel() * 8), "ms_per_step": e2e_s * 1e3,
+           "ms_per_step_min": min(e2e_each) * 1e3, "ms_per_step_median": float(np.median(e2e_each)) * 1e3,
+           "steps": e2e_steps, "warmup": e2e_warmup,
            "timing": "host perf_counter around synchronous sttsv_apply_host (pinned buffers; only the %d active "
                      "entries of x and y cross PCIe, the host zero-fills y during the GPU work)" % info["n_active"]
                      if sparse_x else
@@ -385,7 +395,7 @@ def run_ours(args):
         dxh = torch.from_numpy(dhg.x.copy()).pin_memory()
         dyh = torch.empty(dhg.n, dtype=torch.float64).pin_memory()
         dx_np, dy_np = dxh.numpy(), dyh.numpy()
-        for _ in range(3):
+        for _ in range(e2e_warmup):
             dplan.apply_host(dx_np, dy_np)
         t0 = time.perf_counter()
         for _ in range(e2e_steps):

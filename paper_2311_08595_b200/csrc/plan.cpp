@@ -1300,7 +1300,7 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
     const int32_t* act = p->h_act.data();
     double* xa = p->h_xa;
     double* ya = p->h_xa + na;
-#pragma omp parallel for schedule(static) if (na > 16384)
+#pragma omp parallel for schedule(dynamic, 2048) if (na > 16384)
     for (int64_t i = 0; i < na; ++i) xa[i] = x_host[act[i]];
     sttsv_status_t st0 = check_async(p);
     if (st0 != STTSV_OK) return st0;
@@ -1311,13 +1311,15 @@ extern "C" sttsv_status_t sttsv_apply_host(sttsv_plan_t p, const double* x_host,
     if (st != STTSV_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(ya, p->d_ya, (size_t)na * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H y_a");
     const int64_t n = p->n;
-#pragma omp parallel for schedule(static) if (n > (1 << 20))
+    // dynamic: a descheduled thread must not hold its share of the 8n bytes back (static
+    // scheduling showed 1-5 ms outliers on a 0.32 ms call, tools/e2e_diag.py)
+#pragma omp parallel for schedule(dynamic, 1) if (n > (1 << 20))
     for (int64_t c = 0; c < (n + 65535) / 65536; ++c) {
       const int64_t a = c * 65536, b = std::min<int64_t>(n, a + 65536);
       memset(y_host + a, 0, (size_t)(b - a) * sizeof(double));
     }
     CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
-#pragma omp parallel for schedule(static) if (na > 16384)
+#pragma omp parallel for schedule(dynamic, 2048) if (na > 16384)
     for (int64_t i = 0; i < na; ++i) y_host[act[i]] = ya[i];
     return STTSV_OK;
   }
